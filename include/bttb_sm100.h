@@ -1,0 +1,110 @@
+/*
+ * bttb_sm100.h -- C ABI of the B200-native (sm_100a) fast BTTB forward operator.
+ *
+ * Drop-in boundary for the hot path of the reference package `bttb`
+ * (arXiv 1912.06976; /root/reference/pkg/src/bttb).  The reference has no FFI
+ * of its own: its boundary is a pure-Python function API.  Each entry point
+ * below replaces one reference function; the Python mirror in
+ * paper_1912_06976_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *  - Every call returns BTTB_OK (0) or a negative status; the message of the
+ *    last failure on the calling thread is in bttb_last_error().
+ *  - Vectors are C-contiguous float64 (plan dtype F64) or float32 (F32) in the
+ *    reference ordering (multiply.py:25-26): model = layer-major, x-fastest
+ *    (prism (p,q) of layer r at r*n_r + q*nx + p); data = x-fastest (j*sx + i).
+ *  - The plan owns all device memory it allocates; callers own x and y.
+ *  - Plans are safe to share across threads: bttb_apply serialises on a
+ *    per-plan mutex (the reference's apply is reentrant, README.md:120-122).
+ */
+#ifndef BTTB_SM100_H
+#define BTTB_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { BTTB_OK = 0, BTTB_EINVAL = -1, BTTB_ECUDA = -2, BTTB_ENONFINITE = -3, BTTB_ENOMEM = -4 };
+enum { BTTB_GRAVITY = 0, BTTB_MAGNETIC = 1 };
+enum { BTTB_F64 = 0, BTTB_F32 = 1 };
+enum { BTTB_FORWARD = 0, BTTB_TRANSPOSE = 1 };
+enum { BTTB_DEVICE_PTR = 0, BTTB_HOST_PTR = 1 };
+
+/* Geometry; mirrors GridSpec (grid.py:26-104).  z_blocks has nz+1 entries. */
+typedef struct {
+  int64_t sx, sy, nz, pxl, pxr, pyl, pyr;
+  double dx, dy;
+  const double* z_blocks;
+} bttb_grid;
+
+/* Kernel constants; mirrors KernelParams (kernels.py:19-45):
+ * gravity -> gamma_scaled = gamma*scale (kernels.py:98);
+ * magnetic -> gc = magnetic_constants(D, I, F) (kernels.py:48-64). */
+typedef struct {
+  int kind;
+  double gamma_scaled;
+  double gc[5];
+} bttb_kernel;
+
+typedef struct bttb_plan_s bttb_plan;
+
+/* Replaces build_transform_stack (transform.py:91-104): generates every
+ * layer's kernel entries on the GPU (kernels.py:158-184), embeds them
+ * (transform.py:85-88) at FFT lengths Lx >= sx+nx-1, Ly >= sy+ny-1 (0 = pick
+ * automatically) and caches one half spectrum per layer in HBM.  The plan
+ * holds layers [layer_begin, layer_end) of the grid (layer sharding across
+ * GPUs; pass 0, nz for all).  Returns BTTB_ENONFINITE with the reference's
+ * FloatingPointError text (kernels.py:74-78) if an entry is not finite. */
+int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype, int device,
+                     int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly);
+
+int bttb_plan_destroy(bttb_plan* plan);
+
+/* Replaces apply(stack, x, mode) (multiply.py:22-58) for `batch` vectors.
+ * FORWARD: x = batch x (n_r * local layers), y = batch x m (the partial
+ *          sum over the plan's layers; overwritten).
+ * TRANSPOSE: x = batch x m, y = batch x (n_r * local layers).
+ * where = BTTB_DEVICE_PTR (x, y in device memory of the plan's GPU; runs
+ * asynchronously on `stream`, a cudaStream_t or NULL) or BTTB_HOST_PTR
+ * (host memory; copies in and out, synchronous). */
+int bttb_apply(bttb_plan* plan, int mode, const void* x, void* y, int64_t batch, int where, void* stream);
+
+/* Entry-generator parity hook: the layer's response window, shape
+ * (sx+nx-1) x (sy+ny-1), row-major, as layer_response_window returns it
+ * (kernels.py:158-184).  `layer` is a global layer index. */
+int bttb_layer_window(bttb_plan* plan, int64_t layer, double* host_out);
+
+/* Copy the cached half spectrum of a local layer (Hx x Ly complex, as stored:
+ * scaled by 1/(Lx*Ly), dtype of the plan) to host memory. */
+int bttb_layer_spectrum(bttb_plan* plan, int64_t local_layer, void* host_out);
+
+/* Plan facts: info[0..9] = Lx, Ly, Hx, layer_begin, layer_end, dtype, kind,
+ * layers per chunk, batch per group, kernels launched by the last apply. */
+int bttb_plan_info(const bttb_plan* plan, int64_t* info);
+
+/* Replace gravity_layer_response (kernels.py:81-102) and magnetic_response
+ * (kernels.py:105-155) over arbitrary corner vectors x (ncx) and y (ncy):
+ * out is (ncx-1) x (ncy-1), row-major, host memory.  xy / r2 are the
+ * DistanceTables arrays (ncx x ncy) or NULL to form them as x*y, x*x+y*y. */
+int bttb_gravity_response(const double* x, int64_t ncx, const double* y, int64_t ncy, const double* xy,
+                          const double* r2, double z1, double z2, double gamma_scaled, double* out, int device);
+int bttb_magnetic_response(const double* x, int64_t ncx, const double* y, int64_t ncy, const double* r2,
+                           double z1, double z2, const double* gc, double* out, int device);
+
+/* Smallest supported FFT length >= n (2^a, a>=3; 2^a*3^b or 2^a*5^b with
+ * a>=2, b>=1; at most 8192), or -1. */
+int64_t bttb_fft_length(int64_t n);
+
+/* Last error message on the calling thread ("" if none). */
+const char* bttb_last_error(void);
+
+/* Library version string. */
+const char* bttb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BTTB_SM100_H */

@@ -1,0 +1,719 @@
+// C ABI (include/bttb_sm100.h): plan = the device-resident spectrum cache plus
+// the launch schedule of the fused forward / transpose operator.
+//
+// Reference counterparts: build_transform_stack (transform.py:91-104),
+// apply (multiply.py:22-58), layer_response_window (kernels.py:158-184),
+// gravity_layer_response / magnetic_response (kernels.py:81-155).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bttb_sm100.h"
+#include "entries.h"
+#include "spectral.h"
+
+using namespace bttb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return fail(BTTB_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                       \
+  } while (0)
+
+// --- FFT length family and radix plans ------------------------------------
+int length_family(int64_t L) {  // returns E (elements per thread) or 0
+  if (L < 8 || L > 8192) return 0;
+  int64_t t = L;
+  int a = 0, b = 0, c = 0;
+  while (t % 2 == 0) { t /= 2; ++a; }
+  while (t % 3 == 0) { t /= 3; ++b; }
+  while (t % 5 == 0) { t /= 5; ++c; }
+  if (t != 1) return 0;
+  if (b == 0 && c == 0 && a >= 3) return 8;
+  if (c == 0 && a >= 2 && b >= 1) return 12;
+  if (b == 0 && a >= 2 && c >= 1) return 20;
+  return 0;
+}
+
+int64_t pick_length(int64_t n) {
+  for (int64_t L = std::max<int64_t>(n, 8); L <= 8192; ++L)
+    if (length_family(L)) return L;
+  return -1;
+}
+
+struct FFTPlanHost {
+  int L = 0, E = 0, nt = 0, npass = 0;
+  int radix[8] = {0};
+  double2* tw64 = nullptr;
+  float2* tw32 = nullptr;
+
+  int init(int64_t len) {
+    L = (int)len;
+    E = length_family(len);
+    if (!E) return fail(BTTB_EINVAL, "unsupported FFT length %lld", (long long)len);
+    nt = L / E;
+    static const int cand8[] = {8, 4, 2, 0}, cand12[] = {12, 6, 4, 3, 2, 0}, cand20[] = {20, 10, 5, 4, 2, 0};
+    const int* cand = E == 8 ? cand8 : E == 12 ? cand12 : cand20;
+    int rem = L;
+    npass = 0;
+    while (rem > 1) {
+      int r = 0;
+      for (const int* p = cand; *p; ++p)
+        if (rem % *p == 0) { r = *p; break; }
+      if (!r || npass == 8) return fail(BTTB_EINVAL, "no radix plan for length %d", L);
+      radix[npass++] = r;
+      rem /= r;
+    }
+    std::vector<double2> h64(L);
+    std::vector<float2> h32(L);
+    for (int m = 0; m < L; ++m) {
+      // exp(-2 pi i m / L), evaluated in extended precision then rounded
+      const long double ang = 2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)L;
+      const long double c = cosl(ang), s = -sinl(ang);
+      h64[m] = make_double2((double)c, (double)s);
+      h32[m] = make_float2((float)c, (float)s);
+    }
+    CU(cudaMalloc(&tw64, sizeof(double2) * L));
+    CU(cudaMalloc(&tw32, sizeof(float2) * L));
+    CU(cudaMemcpy(tw64, h64.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(tw32, h32.data(), sizeof(float2) * L, cudaMemcpyHostToDevice));
+    return BTTB_OK;
+  }
+  void release() {
+    if (tw64) cudaFree(tw64);
+    if (tw32) cudaFree(tw32);
+    tw64 = nullptr;
+    tw32 = nullptr;
+  }
+  template <class T> FFTDesc<T> desc() const {
+    FFTDesc<T> d;
+    if constexpr (std::is_same<T, double>::value) d.tw = tw64; else d.tw = tw32;
+    d.L = L;
+    d.nt = nt;
+    d.npass = npass;
+    d.code = 0;
+    for (int i = 0; i < npass; ++i) d.code |= radix_code(radix[i]) << (4 * i);
+    return d;
+  }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t n) {
+    if (n <= bytes) return BTTB_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) return fail(BTTB_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", n, cudaGetErrorString(e));
+    bytes = n;
+    return BTTB_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+size_t chunk_budget() {
+  const char* env = getenv("BTTB_CHUNK_BYTES");
+  if (env) return (size_t)atoll(env);
+  return (size_t)48 << 20;
+}
+
+}  // namespace
+
+struct bttb_plan_s {
+  int device = 0, dtype = BTTB_F64, kind = BTTB_GRAVITY;
+  int64_t sx = 0, sy = 0, nz = 0, pxl = 0, pxr = 0, pyl = 0, pyr = 0, nx = 0, ny = 0, mx = 0, my = 0;
+  double dx = 0, dy = 0;
+  std::vector<double> z;
+  int64_t l0 = 0, l1 = 0, nzl = 0;
+  double gs = 0, gc[5] = {0, 0, 0, 0, 0};
+  int64_t Lx = 0, Ly = 0, Hx = 0;
+  FFTPlanHost fx, fy;
+  size_t elem = 16;
+  void* spectra = nullptr;
+  DevBuf ybuf, wbuf, hin, hout;
+  int64_t last_K = 0, last_G = 0, last_launches = 0;
+  std::mutex mu;
+
+  int64_t n_r() const { return nx * ny; }
+  int64_t m() const { return sx * sy; }
+  int64_t nloc() const { return n_r() * nzl; }
+};
+
+namespace {
+
+// corner vectors exactly as the reference forms its distance tables
+void corner_vectors(const bttb_plan_s* p, std::vector<double>& cx, std::vector<double>& cy) {
+  if (p->kind == BTTB_GRAVITY) {  // sym_distances, grid.py:177-187
+    const int64_t lx = p->sx + std::max(p->pxl, p->pxr) + 1, ly = p->sy + std::max(p->pyl, p->pyr) + 1;
+    cx.resize(lx);
+    cy.resize(ly);
+    for (int64_t l = 0; l < lx; ++l) cx[l] = ((double)l - 0.5) * p->dx;
+    for (int64_t l = 0; l < ly; ++l) cy[l] = ((double)l - 0.5) * p->dy;
+  } else {  // full_distances sliced to the window, grid.py:190-199 + kernels.py:178-183
+    cx.resize(p->mx + 1);
+    cy.resize(p->my + 1);
+    for (int64_t c = 0; c <= p->mx; ++c) cx[c] = ((double)(c - p->sx - p->pxl) + 0.5) * p->dx;
+    for (int64_t c = 0; c <= p->my; ++c) cy[c] = ((double)(c - p->sy - p->pyl) + 0.5) * p->dy;
+  }
+}
+
+struct EntryScratch {
+  DevBuf cx, cy, cm, mag, flag;
+  int ncx = 0, ncy = 0;
+  MagCorners mc{};
+  int init(const std::vector<double>& hx, const std::vector<double>& hy, int kind) {
+    ncx = (int)hx.size();
+    ncy = (int)hy.size();
+    const size_t nc = (size_t)ncx * ncy;
+    int rc;
+    if ((rc = cx.ensure(sizeof(double) * ncx)) || (rc = cy.ensure(sizeof(double) * ncy)) ||
+        (rc = flag.ensure(sizeof(int))))
+      return rc;
+    CU(cudaMemcpy(cx.p, hx.data(), sizeof(double) * ncx, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(cy.p, hy.data(), sizeof(double) * ncy, cudaMemcpyHostToDevice));
+    CU(cudaMemset(flag.p, 0, sizeof(int)));
+    if (kind == BTTB_GRAVITY) {
+      if ((rc = cm.ensure(sizeof(double) * nc))) return rc;
+    } else {
+      if ((rc = mag.ensure(sizeof(double) * nc * 6))) return rc;
+      double* b = static_cast<double*>(mag.p);
+      mc = MagCorners{b, b + nc, b + 2 * nc, b + 3 * nc, b + 4 * nc, b + 5 * nc};
+    }
+    return BTTB_OK;
+  }
+  void release() {
+    cx.release();
+    cy.release();
+    cm.release();
+    mag.release();
+    flag.release();
+  }
+};
+
+const char* kind_name(int kind) { return kind == BTTB_GRAVITY ? "gravity" : "magnetic"; }
+
+int check_flag(EntryScratch& s, int kind) {
+  int h = 0;
+  CU(cudaMemcpy(&h, s.flag.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h)
+    return fail(BTTB_ENONFINITE,
+                "non-finite value in %s response; staggered distances should make this impossible",
+                kind_name(kind));
+  return BTTB_OK;
+}
+
+EmbedArgs embed_args(const bttb_plan_s* p) {
+  EmbedArgs a;
+  a.kind = p->kind;
+  a.sx = (int)p->sx;
+  a.sy = (int)p->sy;
+  a.nx = (int)p->nx;
+  a.ny = (int)p->ny;
+  a.pxl = (int)p->pxl;
+  a.pyl = (int)p->pyl;
+  a.Lx = (int)p->Lx;
+  a.Ly = (int)p->Ly;
+  return a;
+}
+
+GC5 gc5(const bttb_plan_s* p) {
+  GC5 g;
+  for (int i = 0; i < 5; ++i) g.v[i] = p->gc[i];
+  return g;
+}
+
+int layer_corners(bttb_plan_s* p, EntryScratch& s, int64_t layer, cudaStream_t st) {
+  const double z1 = p->z[layer], z2 = p->z[layer + 1];
+  CU(launch_corners(p->kind, (const double*)s.cx.p, s.ncx, (const double*)s.cy.p, s.ncy, nullptr, nullptr, z1, z2,
+                    p->gs, (double*)s.cm.p, s.mc, st));
+  return BTTB_OK;
+}
+
+int build_spectra(bttb_plan_s* p) {
+  std::vector<double> hx, hy;
+  corner_vectors(p, hx, hy);
+  EntryScratch s;
+  int rc = s.init(hx, hy, p->kind);
+  DevBuf emb, yb;
+  if (!rc) rc = emb.ensure(sizeof(double) * p->Lx * p->Ly);
+  if (!rc) rc = yb.ensure(sizeof(double2) * p->Hx * p->Ly);
+  if (rc) {
+    s.release();
+    return rc;
+  }
+  cudaStream_t st = 0;
+  const EmbedArgs ea = embed_args(p);
+  const FFTDesc<double> dx = p->fx.desc<double>(), dy = p->fy.desc<double>();
+  const double scale = 1.0 / ((double)p->Lx * (double)p->Ly);
+  for (int64_t r = 0; r < p->nzl && !rc; ++r) {
+    const int64_t g = p->l0 + r;
+    rc = layer_corners(p, s, g, st);
+    if (rc) break;
+    cudaError_t e = launch_embed(ea, (const double*)s.cm.p, s.mc, (const double*)s.cx.p, (const double*)s.cy.p,
+                                 s.ncy, p->z[g], p->z[g + 1], gc5(p), (int*)s.flag.p, (double*)emb.p, st);
+    if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "embed: %s", cudaGetErrorString(e)); break; }
+    RowR2CArgs ra{};
+    ra.in = emb.p;
+    ra.in_bstride = 0;
+    ra.in_sstride = 0;
+    ra.spb = 1;
+    ra.ld_in = (int)p->Lx;
+    ra.nrows = (int)p->Ly;
+    ra.nvalid = (int)p->Lx;
+    ra.nslabs = 1;
+    ra.out = yb.p;
+    ra.out_sstride = 0;
+    ra.ld_out = (int)p->Ly;
+    ra.Hx = (int)p->Hx;
+    e = launch_row_r2c<double>(ra, dx, p->fx.E, st);
+    if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "build row pass: %s", cudaGetErrorString(e)); break; }
+    ColSpecArgs ca{};
+    ca.Y = yb.p;
+    ca.ldy = (int)p->Ly;
+    ca.S = static_cast<char*>(p->spectra) + (size_t)r * p->Hx * p->Ly * p->elem;
+    ca.lds = (int)p->Ly;
+    ca.Hx = (int)p->Hx;
+    ca.scale = scale;
+    e = p->dtype == BTTB_F64 ? launch_col_spec<double>(ca, dy, p->fy.E, st)
+                             : launch_col_spec<float>(ca, dy, p->fy.E, st);
+    if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "build column pass: %s", cudaGetErrorString(e)); break; }
+  }
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(BTTB_ECUDA, "spectrum build: %s", cudaGetErrorString(e));
+  }
+  if (!rc) rc = check_flag(s, p->kind);
+  s.release();
+  emb.release();
+  yb.release();
+  return rc;
+}
+
+template <class T>
+int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st) {
+  using V = cplx<T>;
+  const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
+  const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
+                nloc = p->nloc();
+  const size_t slab = (size_t)Hx * ny * sizeof(V);
+  const size_t budget = chunk_budget();
+  int64_t K = std::max<int64_t>(1, std::min<int64_t>(p->nzl, (int64_t)(budget / slab)));
+  int64_t G = 1;
+  if (K == p->nzl) G = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(budget / (slab * p->nzl))));
+  int rc;
+  if ((rc = p->ybuf.ensure(slab * K * G))) return rc;
+  if ((rc = p->wbuf.ensure((size_t)Hx * sy * sizeof(V) * G))) return rc;
+  p->last_K = K;
+  p->last_G = G;
+  int64_t launches = 0;
+  V* Yb = static_cast<V*>(p->ybuf.p);
+  V* Wb = static_cast<V*>(p->wbuf.p);
+  const V* S = static_cast<const V*>(p->spectra);
+  const long long s_rstride = (long long)Hx * p->Ly;
+  for (int64_t b0 = 0; b0 < batch; b0 += G) {
+    const int gb = (int)std::min<int64_t>(G, batch - b0);
+    if (mode == BTTB_FORWARD) {
+      const T* xin = static_cast<const T*>(x) + b0 * nloc;
+      for (int64_t r0 = 0; r0 < p->nzl; r0 += K) {
+        const int k = (int)std::min<int64_t>(K, p->nzl - r0);
+        RowR2CArgs ra{};
+        ra.in = xin + r0 * n_r;
+        ra.in_bstride = nloc;
+        ra.in_sstride = n_r;
+        ra.spb = k;
+        ra.ld_in = (int)nx;
+        ra.nrows = (int)ny;
+        ra.nvalid = (int)nx;
+        ra.nslabs = gb * k;
+        ra.out = Yb;
+        ra.out_sstride = (long long)Hx * ny;
+        ra.ld_out = (int)ny;
+        ra.Hx = (int)Hx;
+        CU(launch_row_r2c<T>(ra, dx, p->fx.E, st));
+        ColFwdArgs ca{};
+        ca.Y = Yb;
+        ca.y_bstride = (long long)k * Hx * ny;
+        ca.y_rstride = (long long)Hx * ny;
+        ca.ldy = (int)ny;
+        ca.nvalid = (int)ny;
+        ca.S = S + r0 * s_rstride;
+        ca.s_rstride = s_rstride;
+        ca.lds = (int)p->Ly;
+        ca.K = k;
+        ca.W = Wb;
+        ca.w_bstride = (long long)Hx * sy;
+        ca.ldw = (int)sy;
+        ca.nout = (int)sy;
+        ca.accumulate = r0 > 0;
+        ca.Hx = (int)Hx;
+        ca.nbatch = gb;
+        CU(launch_col_fwd<T>(ca, dy, p->fy.E, st));
+        launches += 2;
+      }
+      RowC2RArgs oa{};
+      oa.in = Wb;
+      oa.in_sstride = (long long)Hx * sy;
+      oa.ld_in = (int)sy;
+      oa.nrows = (int)sy;
+      oa.Hx = (int)Hx;
+      oa.nslabs = gb;
+      oa.out = static_cast<T*>(y) + b0 * m;
+      oa.out_bstride = m;
+      oa.out_sstride = 0;
+      oa.spb = 1;
+      oa.ld_out = (int)sx;
+      oa.nout = (int)sx;
+      CU(launch_row_c2r<T>(oa, dx, p->fx.E, st));
+      launches += 1;
+    } else {
+      RowR2CArgs ra{};
+      ra.in = static_cast<const T*>(x) + b0 * m;
+      ra.in_bstride = m;
+      ra.in_sstride = 0;
+      ra.spb = 1;
+      ra.ld_in = (int)sx;
+      ra.nrows = (int)sy;
+      ra.nvalid = (int)sx;
+      ra.nslabs = gb;
+      ra.out = Wb;
+      ra.out_sstride = (long long)Hx * sy;
+      ra.ld_out = (int)sy;
+      ra.Hx = (int)Hx;
+      CU(launch_row_r2c<T>(ra, dx, p->fx.E, st));
+      launches += 1;
+      T* yout = static_cast<T*>(y) + b0 * nloc;
+      for (int64_t r0 = 0; r0 < p->nzl; r0 += K) {
+        const int k = (int)std::min<int64_t>(K, p->nzl - r0);
+        ColTraArgs ca{};
+        ca.D = Wb;
+        ca.d_bstride = (long long)Hx * sy;
+        ca.ldd = (int)sy;
+        ca.nvalid = (int)sy;
+        ca.S = S + r0 * s_rstride;
+        ca.s_rstride = s_rstride;
+        ca.lds = (int)p->Ly;
+        ca.K = k;
+        ca.W = Yb;
+        ca.w_bstride = (long long)k * Hx * ny;
+        ca.w_rstride = (long long)Hx * ny;
+        ca.ldw = (int)ny;
+        ca.nout = (int)ny;
+        ca.Hx = (int)Hx;
+        ca.nbatch = gb;
+        CU(launch_col_tra<T>(ca, dy, p->fy.E, st));
+        RowC2RArgs oa{};
+        oa.in = Yb;
+        oa.in_sstride = (long long)Hx * ny;
+        oa.ld_in = (int)ny;
+        oa.nrows = (int)ny;
+        oa.Hx = (int)Hx;
+        oa.nslabs = gb * k;
+        oa.out = yout + r0 * n_r;
+        oa.out_bstride = nloc;
+        oa.out_sstride = n_r;
+        oa.spb = k;
+        oa.ld_out = (int)nx;
+        oa.nout = (int)nx;
+        CU(launch_row_c2r<T>(oa, dx, p->fx.E, st));
+        launches += 2;
+      }
+    }
+  }
+  p->last_launches = launches;
+  return BTTB_OK;
+}
+
+void destroy_plan(bttb_plan_s* p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  if (p->spectra) cudaFree(p->spectra);
+  p->fx.release();
+  p->fy.release();
+  p->ybuf.release();
+  p->wbuf.release();
+  p->hin.release();
+  p->hout.release();
+  delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bttb_last_error(void) { return g_err.c_str(); }
+
+const char* bttb_version(void) { return "bttb_sm100 0.1.0 (sm_100a)"; }
+
+int64_t bttb_fft_length(int64_t n) { return pick_length(n); }
+
+int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype, int device,
+                     int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly) {
+  g_err.clear();
+  if (!out || !grid || !kernel) return fail(BTTB_EINVAL, "null argument");
+  *out = nullptr;
+  if (grid->sx < 1 || grid->sy < 1 || grid->nz < 1) return fail(BTTB_EINVAL, "sx, sy, nz must be positive");
+  if (grid->pxl < 0 || grid->pxr < 0 || grid->pyl < 0 || grid->pyr < 0)
+    return fail(BTTB_EINVAL, "padding must be non-negative");
+  if (!(grid->dx > 0) || !(grid->dy > 0)) return fail(BTTB_EINVAL, "dx, dy must be positive");
+  if (!grid->z_blocks) return fail(BTTB_EINVAL, "z_blocks is null");
+  if (kernel->kind != BTTB_GRAVITY && kernel->kind != BTTB_MAGNETIC) return fail(BTTB_EINVAL, "unknown kernel kind");
+  if (dtype != BTTB_F64 && dtype != BTTB_F32) return fail(BTTB_EINVAL, "unknown dtype");
+  if (layer_begin < 0 || layer_end > grid->nz || layer_begin >= layer_end)
+    return fail(BTTB_EINVAL, "layer range [%lld, %lld) outside [0, %lld)", (long long)layer_begin,
+                (long long)layer_end, (long long)grid->nz);
+  for (int64_t r = 0; r < grid->nz; ++r) {
+    const double z1 = grid->z_blocks[r], z2 = grid->z_blocks[r + 1];
+    if (z2 < z1) return fail(BTTB_EINVAL, "layer depths must satisfy z2 >= z1, got (%g, %g)", z1, z2);
+    if (z1 < 0) return fail(BTTB_EINVAL, "layer top must satisfy z1 >= 0, got %g", z1);
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(BTTB_ECUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(BTTB_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  DeviceGuard dg(device);
+  bttb_plan_s* p = new bttb_plan_s();
+  p->device = device;
+  p->dtype = dtype;
+  p->kind = kernel->kind;
+  p->sx = grid->sx; p->sy = grid->sy; p->nz = grid->nz;
+  p->pxl = grid->pxl; p->pxr = grid->pxr; p->pyl = grid->pyl; p->pyr = grid->pyr;
+  p->nx = p->sx + p->pxl + p->pxr;
+  p->ny = p->sy + p->pyl + p->pyr;
+  p->mx = p->sx + p->nx - 1;
+  p->my = p->sy + p->ny - 1;
+  p->dx = grid->dx;
+  p->dy = grid->dy;
+  p->z.assign(grid->z_blocks, grid->z_blocks + grid->nz + 1);
+  p->l0 = layer_begin;
+  p->l1 = layer_end;
+  p->nzl = layer_end - layer_begin;
+  p->gs = kernel->gamma_scaled;
+  for (int i = 0; i < 5; ++i) p->gc[i] = kernel->gc[i];
+  p->Lx = Lx > 0 ? Lx : pick_length(p->mx);
+  p->Ly = Ly > 0 ? Ly : pick_length(p->my);
+  int rc = BTTB_OK;
+  if (p->Lx < p->mx || p->Ly < p->my || !length_family(p->Lx) || !length_family(p->Ly)) {
+    rc = fail(BTTB_EINVAL, "FFT lengths (%lld, %lld) unsupported for embedding (%lld, %lld)", (long long)p->Lx,
+              (long long)p->Ly, (long long)p->mx, (long long)p->my);
+  }
+  if (!rc) {
+    p->Hx = p->Lx / 2 + 1;
+    p->elem = dtype == BTTB_F64 ? sizeof(double2) : sizeof(float2);
+    rc = p->fx.init(p->Lx);
+  }
+  if (!rc) rc = p->fy.init(p->Ly);
+  if (!rc) {
+    const size_t bytes = (size_t)p->nzl * p->Hx * p->Ly * p->elem;
+    e = cudaMalloc(&p->spectra, bytes);
+    if (e != cudaSuccess) {
+      p->spectra = nullptr;
+      rc = fail(BTTB_ENOMEM, "cannot allocate %zu bytes of spectrum cache: %s", bytes, cudaGetErrorString(e));
+    }
+  }
+  if (!rc) rc = build_spectra(p);
+  if (rc) {
+    std::string msg = g_err;
+    destroy_plan(p);
+    g_err = msg;
+    return rc;
+  }
+  *out = p;
+  return BTTB_OK;
+}
+
+int bttb_plan_destroy(bttb_plan* plan) {
+  destroy_plan(plan);
+  return BTTB_OK;
+}
+
+int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, int where, void* stream) {
+  g_err.clear();
+  if (!p || !x || !y) return fail(BTTB_EINVAL, "null argument");
+  if (mode != BTTB_FORWARD && mode != BTTB_TRANSPOSE)
+    return fail(BTTB_EINVAL, "mode must be 'forward' or 'transpose', got %d", mode);
+  if (batch < 0) return fail(BTTB_EINVAL, "batch must be >= 0");
+  if (batch == 0) return BTTB_OK;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t in_elems = (size_t)batch * (mode == BTTB_FORWARD ? p->nloc() : p->m());
+  const size_t out_elems = (size_t)batch * (mode == BTTB_FORWARD ? p->m() : p->nloc());
+  const size_t esz = p->elem / 2;
+  const void* xd = x;
+  void* yd = y;
+  if (where == BTTB_HOST_PTR) {
+    int rc;
+    if ((rc = p->hin.ensure(in_elems * esz)) || (rc = p->hout.ensure(out_elems * esz))) return rc;
+    CU(cudaMemcpyAsync(p->hin.p, x, in_elems * esz, cudaMemcpyHostToDevice, st));
+    xd = p->hin.p;
+    yd = p->hout.p;
+  } else if (where != BTTB_DEVICE_PTR) {
+    return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR or BTTB_HOST_PTR");
+  }
+  int rc = p->dtype == BTTB_F64 ? run_apply<double>(p, mode, xd, yd, batch, st)
+                                : run_apply<float>(p, mode, xd, yd, batch, st);
+  if (rc) return rc;
+  if (where == BTTB_HOST_PTR) {
+    CU(cudaMemcpyAsync(y, yd, out_elems * esz, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  return BTTB_OK;
+}
+
+int bttb_layer_window(bttb_plan* p, int64_t layer, double* host_out) {
+  g_err.clear();
+  if (!p || !host_out) return fail(BTTB_EINVAL, "null argument");
+  if (layer < 0 || layer >= p->nz) return fail(BTTB_EINVAL, "layer %lld out of range", (long long)layer);
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard dg(p->device);
+  std::vector<double> hx, hy;
+  corner_vectors(p, hx, hy);
+  EntryScratch s;
+  DevBuf w;
+  int rc = s.init(hx, hy, p->kind);
+  if (!rc) rc = w.ensure(sizeof(double) * p->mx * p->my);
+  if (!rc) rc = layer_corners(p, s, layer, 0);
+  if (!rc) {
+    cudaError_t e = launch_window(embed_args(p), (int)p->mx, (int)p->my, (const double*)s.cm.p, s.mc,
+                                  (const double*)s.cx.p, (const double*)s.cy.p, s.ncy, p->z[layer],
+                                  p->z[layer + 1], gc5(p), (int*)s.flag.p, (double*)w.p, 0);
+    if (e != cudaSuccess) rc = fail(BTTB_ECUDA, "window: %s", cudaGetErrorString(e));
+  }
+  if (!rc) {
+    cudaError_t e = cudaMemcpy(host_out, w.p, sizeof(double) * p->mx * p->my, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(BTTB_ECUDA, "window copy: %s", cudaGetErrorString(e));
+  }
+  if (!rc) rc = check_flag(s, p->kind);
+  s.release();
+  w.release();
+  return rc;
+}
+
+int bttb_layer_spectrum(bttb_plan* p, int64_t local_layer, void* host_out) {
+  g_err.clear();
+  if (!p || !host_out) return fail(BTTB_EINVAL, "null argument");
+  if (local_layer < 0 || local_layer >= p->nzl) return fail(BTTB_EINVAL, "local layer out of range");
+  DeviceGuard dg(p->device);
+  const size_t bytes = (size_t)p->Hx * p->Ly * p->elem;
+  CU(cudaMemcpy(host_out, static_cast<char*>(p->spectra) + bytes * local_layer, bytes, cudaMemcpyDeviceToHost));
+  return BTTB_OK;
+}
+
+int bttb_plan_info(const bttb_plan* p, int64_t* info) {
+  if (!p || !info) return fail(BTTB_EINVAL, "null argument");
+  info[0] = p->Lx;
+  info[1] = p->Ly;
+  info[2] = p->Hx;
+  info[3] = p->l0;
+  info[4] = p->l1;
+  info[5] = p->dtype;
+  info[6] = p->kind;
+  info[7] = p->last_K;
+  info[8] = p->last_G;
+  info[9] = p->last_launches;
+  return BTTB_OK;
+}
+
+static int raw_response(int kind, const double* x, int64_t ncx, const double* y, int64_t ncy, const double* xy,
+                        const double* r2, double z1, double z2, double gs, const double* gc, double* out,
+                        int device) {
+  g_err.clear();
+  if (!x || !y || !out) return fail(BTTB_EINVAL, "null argument");
+  if (z2 < z1) return fail(BTTB_EINVAL, "layer depths must satisfy z2 >= z1, got (%g, %g)", z1, z2);
+  if (z1 < 0) return fail(BTTB_EINVAL, "layer top must satisfy z1 >= 0, got %g", z1);
+  if (ncx < 2 || ncy < 2) return fail(BTTB_EINVAL, "need at least two corners per axis");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(BTTB_ECUDA, "no CUDA device available");
+  DeviceGuard dg(device);
+  std::vector<double> hx(x, x + ncx), hy(y, y + ncy);
+  EntryScratch s;
+  DevBuf dxy, dr2, dout;
+  int rc = s.init(hx, hy, kind);
+  const size_t nc = (size_t)ncx * ncy;
+  if (!rc && xy) {
+    rc = dxy.ensure(sizeof(double) * nc);
+    if (!rc && cudaMemcpy(dxy.p, xy, sizeof(double) * nc, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = fail(BTTB_ECUDA, "copy xy");
+  }
+  if (!rc && r2) {
+    rc = dr2.ensure(sizeof(double) * nc);
+    if (!rc && cudaMemcpy(dr2.p, r2, sizeof(double) * nc, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = fail(BTTB_ECUDA, "copy r2");
+  }
+  const size_t no = (size_t)(ncx - 1) * (ncy - 1);
+  if (!rc) rc = dout.ensure(sizeof(double) * no);
+  GC5 g{};
+  if (gc)
+    for (int i = 0; i < 5; ++i) g.v[i] = gc[i];
+  if (!rc) {
+    cudaError_t e = launch_corners(kind, (const double*)s.cx.p, s.ncx, (const double*)s.cy.p, s.ncy,
+                                   (const double*)dxy.p, (const double*)dr2.p, z1, z2, gs, (double*)s.cm.p, s.mc, 0);
+    if (e == cudaSuccess)
+      e = launch_entries_raw(kind, (const double*)s.cm.p, s.mc, (const double*)s.cx.p, (const double*)s.cy.p, s.ncx,
+                             s.ncy, z1, z2, g, (int*)s.flag.p, (double*)dout.p, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout.p, sizeof(double) * no, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(BTTB_ECUDA, "response: %s", cudaGetErrorString(e));
+  }
+  if (!rc) rc = check_flag(s, kind);
+  s.release();
+  dxy.release();
+  dr2.release();
+  dout.release();
+  return rc;
+}
+
+int bttb_gravity_response(const double* x, int64_t ncx, const double* y, int64_t ncy, const double* xy,
+                          const double* r2, double z1, double z2, double gamma_scaled, double* out, int device) {
+  return raw_response(BTTB_GRAVITY, x, ncx, y, ncy, xy, r2, z1, z2, gamma_scaled, nullptr, out, device);
+}
+
+int bttb_magnetic_response(const double* x, int64_t ncx, const double* y, int64_t ncy, const double* r2,
+                           double z1, double z2, const double* gc, double* out, int device) {
+  if (!gc) return fail(BTTB_EINVAL, "null gc");
+  return raw_response(BTTB_MAGNETIC, x, ncx, y, ncy, nullptr, r2, z1, z2, 0.0, gc, out, device);
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+// Shared-memory Stockham FFT engine for sm_100a (fp64 and fp32).
+//
+// One "team" of nt = L/E threads transforms one length-L complex sequence.
+// Thread t of a team always owns the E elements {t + nt*s : s < E} of the
+// sequence: it loads them straight from global memory before the first
+// radix pass and, because the last Stockham pass of a length-L transform
+// writes element (j + r*L/R) from butterfly j's r-th output, it also ends up
+// holding exactly those elements of the RESULT in registers.  Only the
+// exchanges between passes go through shared memory.  That property is what
+// lets the fused operator kernels multiply by the cached spectrum and
+// accumulate across depth layers in registers (see spectral.cu).
+//
+// Radix passes are compile-time DFTs of size R | E (2,3,4,5 and composites
+// 6,8,10,12,16,20); the pass sequence for a length is chosen at plan time.
+// Transform sign is numpy's forward convention exp(-2*pi*i*n*k/L); the
+// inverse is conj(fft(conj(x))) and is never normalised here (the 1/(Lx*Ly)
+// factor is folded into the cached spectra).
+#pragma once
+#include <cuda_runtime.h>
+#include <type_traits>
+
+namespace bttb {
+
+template <class T> struct CT;
+template <> struct CT<double> { using type = double2; };
+template <> struct CT<float> { using type = float2; };
+template <class T> using cplx = typename CT<T>::type;
+
+template <class V> struct ScalarOf;
+template <> struct ScalarOf<double2> { using type = double; };
+template <> struct ScalarOf<float2> { using type = float; };
+
+template <class V, class S>
+__device__ __forceinline__ V mkc(S a, S b) { V r; r.x = a; r.y = b; return r; }
+
+__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 operator-(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 operator+(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 operator-(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+template <class V> __device__ __forceinline__ V cmul(V a, V b) {
+  return mkc<V>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <class V> __device__ __forceinline__ V conjv(V a) { return mkc<V>(a.x, -a.y); }
+template <class V, class S> __device__ __forceinline__ V scalev(V a, S s) { return mkc<V>(a.x * s, a.y * s); }
+// multiply by -i and +i
+template <class V> __device__ __forceinline__ V mul_mi(V a) { return mkc<V>(a.y, -a.x); }
+template <class V> __device__ __forceinline__ V mul_pi(V a) { return mkc<V>(-a.y, a.x); }
+
+// compile-time loop
+template <int I, int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    sfor<I + 1, N>(f);
+  }
+}
+
+template <int R> struct TwR;
+#include "twiddle_consts.h"
+
+// a * w_R^M, w_R = exp(-2*pi*i/R), with the quarter-turn cases exact
+template <int R, int M, class V>
+__device__ __forceinline__ V twc(V a) {
+  constexpr int m = M % R;
+  using S = typename ScalarOf<V>::type;
+  if constexpr (m == 0) {
+    return a;
+  } else if constexpr (4 * m == R) {
+    return mul_mi(a);
+  } else if constexpr (2 * m == R) {
+    return mkc<V>(-a.x, -a.y);
+  } else if constexpr (4 * m == 3 * R) {
+    return mul_pi(a);
+  } else {
+    const S c = (S)TwR<R>::re[m];
+    const S s = (S)TwR<R>::im[m];
+    return mkc<V>(a.x * c - a.y * s, a.x * s + a.y * c);
+  }
+}
+
+template <int R> struct Split {
+  static constexpr int A = (R % 4 == 0 && R != 4) ? 4 : (R % 2 == 0 && R != 2) ? 2 : (R % 3 == 0 && R != 3) ? 3 : 5;
+  static constexpr int B = R / A;
+};
+
+// In-place forward DFT of size R on x[0..R) (natural order in and out).
+template <int R, class V>
+__device__ __forceinline__ void dft(V* x) {
+  using S = typename ScalarOf<V>::type;
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    V a = x[0], b = x[1];
+    x[0] = a + b;
+    x[1] = a - b;
+  } else if constexpr (R == 3) {
+    const S s3 = (S)0.8660254037844386;
+    V t1 = x[1] + x[2];
+    V t2 = mkc<V>(x[0].x - (S)0.5 * t1.x, x[0].y - (S)0.5 * t1.y);
+    V d = x[1] - x[2];
+    V m = mkc<V>(s3 * d.y, -s3 * d.x);  // -i*s3*d
+    x[0] = x[0] + t1;
+    x[1] = t2 + m;
+    x[2] = t2 - m;
+  } else if constexpr (R == 4) {
+    V t0 = x[0] + x[2], t1 = x[0] - x[2];
+    V t2 = x[1] + x[3], t3 = mul_mi(x[1] - x[3]);
+    x[0] = t0 + t2;
+    x[2] = t0 - t2;
+    x[1] = t1 + t3;
+    x[3] = t1 - t3;
+  } else if constexpr (R == 5) {
+    const S c1 = (S)0.30901699437494745, c2 = (S)-0.8090169943749475;
+    const S s1 = (S)0.9510565162951535, s2 = (S)0.5877852522924731;
+    V t1 = x[1] + x[4], t2 = x[2] + x[3];
+    V t3 = x[1] - x[4], t4 = x[2] - x[3];
+    V a1 = mkc<V>(x[0].x + c1 * t1.x + c2 * t2.x, x[0].y + c1 * t1.y + c2 * t2.y);
+    V a2 = mkc<V>(x[0].x + c2 * t1.x + c1 * t2.x, x[0].y + c2 * t1.y + c1 * t2.y);
+    V b1 = mkc<V>(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y);
+    V b2 = mkc<V>(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y);
+    b1 = mul_mi(b1);
+    b2 = mul_mi(b2);
+    x[0] = x[0] + t1 + t2;
+    x[1] = a1 + b1;
+    x[4] = a1 - b1;
+    x[2] = a2 + b2;
+    x[3] = a2 - b2;
+  } else {
+    // Cooley-Tukey split R = A*B: n = B*n1 + n2, k = k1 + A*k2
+    constexpr int A = Split<R>::A, B = Split<R>::B;
+    V u[R];
+    sfor<0, B>([&](auto n2c) {
+      constexpr int n2 = decltype(n2c)::value;
+      V t[A];
+      sfor<0, A>([&](auto n1c) { constexpr int n1 = decltype(n1c)::value; t[n1] = x[B * n1 + n2]; });
+      dft<A>(t);
+      sfor<0, A>([&](auto k1c) {
+        constexpr int k1 = decltype(k1c)::value;
+        u[n2 * A + k1] = twc<R, n2 * k1>(t[k1]);
+      });
+    });
+    sfor<0, A>([&](auto k1c) {
+      constexpr int k1 = decltype(k1c)::value;
+      V t[B];
+      sfor<0, B>([&](auto n2c) { constexpr int n2 = decltype(n2c)::value; t[n2] = u[n2 * A + k1]; });
+      dft<B>(t);
+      sfor<0, B>([&](auto k2c) { constexpr int k2 = decltype(k2c)::value; x[k1 + A * k2] = t[k2]; });
+    });
+  }
+}
+
+// Plan for one transform length, passed by value to kernels.
+template <class T>
+struct FFTDesc {
+  const cplx<T>* tw;  // tw[m] = exp(-2*pi*i*m/L), m < L
+  int L;              // transform length
+  int nt;             // threads per team = L / E
+  int npass;
+  unsigned code;      // radix of pass p = radix_of((code >> 4p) & 15)
+};
+
+__host__ __device__ inline int radix_of(unsigned c) {
+  switch (c) {
+    case 1: return 2; case 2: return 3; case 3: return 4; case 4: return 5; case 5: return 6;
+    case 6: return 8; case 7: return 10; case 8: return 12; case 9: return 16; case 10: return 20;
+    default: return 0;
+  }
+}
+__host__ __device__ inline unsigned radix_code(int r) {
+  switch (r) {
+    case 2: return 1; case 3: return 2; case 4: return 3; case 5: return 4; case 6: return 5;
+    case 8: return 6; case 10: return 7; case 12: return 8; case 16: return 9; case 20: return 10;
+    default: return 0;
+  }
+}
+
+// One Stockham radix-R pass on the thread's registers (butterflies j = t + nt*b).
+template <class T, int E, int R>
+__device__ __forceinline__ void pass_compute(cplx<T> (&v)[E], int t, int nt, int Ns, int L,
+                                             const cplx<T>* __restrict__ tw) {
+  using V = cplx<T>;
+  constexpr int NB = E / R;
+  const int stride = L / (Ns * R);
+  sfor<0, NB>([&](auto bc) {
+    constexpr int b = decltype(bc)::value;
+    V u[R];
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; u[r] = v[b + r * NB]; });
+    if (Ns > 1) {
+      const int j = t + nt * b;
+      const int k = j % Ns;
+      const int step = k * stride;
+      sfor<1, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        u[r] = cmul(u[r], __ldg(&tw[r * step]));
+      });
+    }
+    dft<R>(u);
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; v[b + r * NB] = u[r]; });
+  });
+}
+
+// Scatter the pass outputs to their Stockham positions in shared memory.
+template <class T, int E, int R>
+__device__ __forceinline__ void pass_store(const cplx<T> (&v)[E], cplx<T>* sm, int t, int nt, int Ns) {
+  constexpr int NB = E / R;
+  sfor<0, NB>([&](auto bc) {
+    constexpr int b = decltype(bc)::value;
+    const int j = t + nt * b;
+    const int k = j % Ns;
+    const int base = (j - k) * R + k;
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; sm[base + r * Ns] = v[b + r * NB]; });
+  });
+}
+
+template <class T, int E>
+__device__ __forceinline__ void run_compute(int R, cplx<T> (&v)[E], int t, int nt, int Ns, int L,
+                                            const cplx<T>* __restrict__ tw) {
+  switch (R) {
+    case 2: if constexpr (E % 2 == 0) pass_compute<T, E, 2>(v, t, nt, Ns, L, tw); break;
+    case 3: if constexpr (E % 3 == 0) pass_compute<T, E, 3>(v, t, nt, Ns, L, tw); break;
+    case 4: if constexpr (E % 4 == 0) pass_compute<T, E, 4>(v, t, nt, Ns, L, tw); break;
+    case 5: if constexpr (E % 5 == 0) pass_compute<T, E, 5>(v, t, nt, Ns, L, tw); break;
+    case 6: if constexpr (E % 6 == 0) pass_compute<T, E, 6>(v, t, nt, Ns, L, tw); break;
+    case 8: if constexpr (E % 8 == 0) pass_compute<T, E, 8>(v, t, nt, Ns, L, tw); break;
+    case 10: if constexpr (E % 10 == 0) pass_compute<T, E, 10>(v, t, nt, Ns, L, tw); break;
+    case 12: if constexpr (E % 12 == 0) pass_compute<T, E, 12>(v, t, nt, Ns, L, tw); break;
+    case 16: if constexpr (E % 16 == 0) pass_compute<T, E, 16>(v, t, nt, Ns, L, tw); break;
+    case 20: if constexpr (E % 20 == 0) pass_compute<T, E, 20>(v, t, nt, Ns, L, tw); break;
+    default: break;
+  }
+}
+
+template <class T, int E>
+__device__ __forceinline__ void run_store(int R, const cplx<T> (&v)[E], cplx<T>* sm, int t, int nt, int Ns) {
+  switch (R) {
+    case 2: if constexpr (E % 2 == 0) pass_store<T, E, 2>(v, sm, t, nt, Ns); break;
+    case 3: if constexpr (E % 3 == 0) pass_store<T, E, 3>(v, sm, t, nt, Ns); break;
+    case 4: if constexpr (E % 4 == 0) pass_store<T, E, 4>(v, sm, t, nt, Ns); break;
+    case 5: if constexpr (E % 5 == 0) pass_store<T, E, 5>(v, sm, t, nt, Ns); break;
+    case 6: if constexpr (E % 6 == 0) pass_store<T, E, 6>(v, sm, t, nt, Ns); break;
+    case 8: if constexpr (E % 8 == 0) pass_store<T, E, 8>(v, sm, t, nt, Ns); break;
+    case 10: if constexpr (E % 10 == 0) pass_store<T, E, 10>(v, sm, t, nt, Ns); break;
+    case 12: if constexpr (E % 12 == 0) pass_store<T, E, 12>(v, sm, t, nt, Ns); break;
+    case 16: if constexpr (E % 16 == 0) pass_store<T, E, 16>(v, sm, t, nt, Ns); break;
+    case 20: if constexpr (E % 20 == 0) pass_store<T, E, 20>(v, sm, t, nt, Ns); break;
+    default: break;
+  }
+}
+
+// Forward FFT of the team's sequence.  v holds elements {t + nt*s} on entry and
+// the same elements of the transform on exit.  sm is the team's L-element
+// shared buffer.  Contains __syncthreads(): every thread of the CTA must call
+// it the same number of times (teams never diverge on the plan).
+template <class T, int E>
+__device__ __forceinline__ void team_fft(cplx<T> (&v)[E], cplx<T>* sm, int t, const FFTDesc<T>& d) {
+  int Ns = 1;
+  for (int p = 0; p < d.npass; ++p) {
+    const int R = radix_of((d.code >> (4 * p)) & 15u);
+    run_compute<T, E>(R, v, t, d.nt, Ns, d.L, d.tw);
+    if (p + 1 < d.npass) {
+      __syncthreads();
+      run_store<T, E>(R, v, sm, t, d.nt, Ns);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < E; ++s) v[s] = sm[t + d.nt * s];
+    }
+    Ns *= R;
+  }
+}
+
+}  // namespace bttb

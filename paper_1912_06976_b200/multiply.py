@@ -1,0 +1,95 @@
+"""Forward and transpose products through the device spectrum cache.
+
+Drop-in for ``/root/reference/pkg/src/bttb/multiply.py``: same ``apply(stack,
+x, mode)`` signature, vector ordering, ValueError messages and a NEW returned
+array (x is never mutated).  Extensions: a leading batch axis, and CUDA torch
+tensors in/out (zero-copy device pointers on the current stream) for
+device-resident iterative use.
+"""
+import numpy as np
+
+from . import _lib
+
+__all__ = ["apply", "relative_error"]
+
+_MODES = {"forward": _lib.FORWARD, "transpose": _lib.TRANSPOSE}
+
+
+def _expected(stack, mode):
+    g = stack.grid
+    if mode == "forward":
+        return stack.n_local, (f"forward expects a vector of length n={stack.n_local} "
+                               f"= nx*ny*nz = {g.nx}*{g.ny}*{stack.nz_local}")
+    return g.m, f"transpose expects a vector of length m={g.m}"
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch") and hasattr(x, "data_ptr")
+
+
+def apply(stack, x, mode, stream=None):
+    """Multiply by the operator (``"forward"``: d = G m) or its transpose.
+
+    x: (n,) / (batch, n) model vectors for forward, (m,) / (batch, m) data
+    vectors for transpose (multiply.py:22-58).  numpy input runs host-to-host
+    through the C ABI and returns a new float64 (fp32 plan: float32) array;
+    a CUDA torch tensor runs device-to-device on ``stream`` (default: the
+    current torch stream) and returns a new tensor.
+    """
+    if mode not in _MODES:
+        raise ValueError(f"mode must be 'forward' or 'transpose', got {mode!r}")
+    want, msg = _expected(stack, mode)
+    other = stack.grid.m if mode == "forward" else stack.n_local
+    if _is_torch(x):
+        return _apply_torch(stack, x, mode, want, other, msg, stream)
+    dt = stack.dtype
+    xa = np.asarray(x, dtype=float)
+    if xa.ndim not in (1, 2) or xa.shape[-1] != want:
+        raise ValueError(f"{msg}, got shape {xa.shape}")
+    batch = 1 if xa.ndim == 1 else xa.shape[0]
+    xin = np.ascontiguousarray(xa, dtype=dt)
+    out = np.empty(xa.shape[:-1] + (other,), dtype=dt)
+    _lib.check(_lib.lib().bttb_apply(stack.handle, _MODES[mode],
+                                     xin.ctypes.data_as(_lib.ctypes.c_void_p),
+                                     out.ctypes.data_as(_lib.ctypes.c_void_p),
+                                     batch, _lib.HOST_PTR, None))
+    return out
+
+
+def _apply_torch(stack, x, mode, want, other, msg, stream):
+    import torch
+
+    if not x.is_cuda:
+        raise ValueError("torch tensors must live on a CUDA device")
+    if x.dim() not in (1, 2) or x.shape[-1] != want:
+        raise ValueError(f"{msg}, got shape {tuple(x.shape)}")
+    tdt = torch.float64 if stack.dtype == np.float64 else torch.float32
+    xin = x.to(dtype=tdt).contiguous()
+    out = torch.empty(tuple(x.shape[:-1]) + (other,), dtype=tdt, device=x.device)
+    batch = 1 if x.dim() == 1 else x.shape[0]
+    st = torch.cuda.current_stream(x.device) if stream is None else stream
+    _lib.check(_lib.lib().bttb_apply(stack.handle, _MODES[mode], _lib.ctypes.c_void_p(xin.data_ptr()),
+                                     _lib.ctypes.c_void_p(out.data_ptr()), batch,
+                                     _lib.DEVICE_PTR, _lib.ctypes.c_void_p(st.cuda_stream)))
+    return out
+
+
+def apply_into(stack, mode, x_ptr, y_ptr, batch=1, stream_ptr=None, host=False):
+    """Raw-pointer entry (bench / multi-GPU driver): y <- op(x), no validation copies."""
+    where = _lib.HOST_PTR if host else _lib.DEVICE_PTR
+    _lib.check(_lib.lib().bttb_apply(stack.handle, _MODES[mode], _lib.ctypes.c_void_p(x_ptr),
+                                     _lib.ctypes.c_void_p(y_ptr), int(batch), where,
+                                     _lib.ctypes.c_void_p(stream_ptr or 0)))
+
+
+def relative_error(a, b):
+    """||a - b|| / ||a||; 0 if both zero, inf if only a is (multiply.py:61-71)."""
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch: {a.shape} vs {b.shape}")
+    na = np.linalg.norm(a)
+    diff = np.linalg.norm(a - b)
+    if na == 0.0:
+        return 0.0 if diff == 0.0 else np.inf
+    return diff / na
