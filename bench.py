@@ -1,0 +1,429 @@
+"""Benchmark of the B200 fast BTTB operator: G*m + G^T*d voxels/s and % HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--dtype f64|f32]
+    python bench.py --impl reference ...        # the reference's CPU path (oracle port)
+
+One step = one forward G*m and one transpose G^T*d over the configured
+workload (BASELINE.json config C4 by default: magnetic, 1000x1000 stations,
+128 layers, 2000x2000 embedding).  Under torchrun every rank holds a
+contiguous block of depth layers (strong scaling: the workload is fixed); the
+forward partial station vectors are summed with one NCCL all-reduce and the
+data vector is broadcast for the transpose (paper_1912_06976_b200/parallel.py).
+
+Rank 0 prints one JSON line (the driver contract in the task statement).
+Roofline: algorithmic bytes per application B = b*(n+m) + b*nz*mx*my
+(SURVEY.md 8(d)), over the measured HBM copy peak in MEASURED_PEAKS.json.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "G·m + Gᵀ·d voxels/sec (fp64/fp32) at 1/2/4/8 B200; % HBM roofline"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def workload(cfg, O):
+    sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, dz, kind, args, batch = O.CONFIGS[cfg]
+    desc = (f"{cfg} {kind} stations {sx}x{sy}, volume {sx + pxl + pxr}x{sy + pyl + pyr}x{nz}, "
+            f"d=({dx:g},{dy:g},{dz:g}) m" + (f", D={args[0]:g} I={args[1]:g} F={args[2]:g}" if args else "")
+            + (f", batch {batch}" if batch > 1 else ""))
+    return desc, batch
+
+
+def algorithmic_bytes(g, b, batch):
+    """B = b*batch*(n+m) + b*nz*mx*my per application."""
+    return b * batch * (g.n + g.m) + b * g.nz * g.mx * g.my
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 6]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm, mx = [], None
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the reference algorithm (oracle port), threads over depth layers
+# ---------------------------------------------------------------------------
+def cpu_sample(cfg, steps, warmup, layers_hint=None):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import bttb_oracle as O
+
+    cores = os.cpu_count() or 1
+    g_full = O.config_grid(cfg)
+    kind, consts = O.config_kernel(cfg)
+    nl = g_full.nz if layers_hint is None else min(g_full.nz, layers_hint)
+    g = O.config_grid(cfg, nz=nl)
+    x, d = O.make_inputs(cfg, g, batch=1)
+    with ThreadPoolExecutor(cores) as pool:
+        t0 = time.perf_counter()
+        fw, tr = O.build_spectra_threaded(g, kind, consts, list(range(nl)), pool)
+        t_build = time.perf_counter() - t0
+        for _ in range(warmup):
+            O.forward_threaded(g, fw, x[0], pool)
+            O.transpose_threaded(g, tr, d[0], pool)
+        tf = tt = 0.0
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.forward_threaded(g, fw, x[0], pool)
+            t1 = time.perf_counter()
+            O.transpose_threaded(g, tr, d[0], pool)
+            tf += t1 - t0
+            tt += time.perf_counter() - t1
+    voxels = g.n  # one batch item of the sample
+    return {"value": voxels * steps / (tf + tt), "unit": "voxels/s", "cores": cores,
+            "sample": (f"{cfg} geometry with {nl} of {g_full.nz} layers, 1 model, numpy pocketfft "
+                       f"(reference algorithm, oracle port), {cores} threads over layers; "
+                       f"build {t_build:.2f}s, fwd {1e3 * tf / steps:.1f} ms, "
+                       f"tra {1e3 * tt / steps:.1f} ms per step"),
+            "fwd_s": tf / steps, "tra_s": tt / steps, "build_s": t_build}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import bttb_oracle as O
+
+    desc, batch = workload(a.config, O)
+    cores = os.cpu_count() or 1
+    sample_layers = min(O.CONFIGS[a.config][2], 2 * cores) if a.config in ("C4", "C5") else None
+    steps = max(1, min(a.steps, 10))
+    warm = max(1, min(a.warmup, 2))
+    r = cpu_sample(a.config, steps, warm, sample_layers)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "voxels/s",
+        "n_gpus": a.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * (r["fwd_s"] + r["tra_s"]), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded (SURVEY.md 8(d))",
+        "config": {"workload": desc, "sample": r["sample"]},
+        "cpu_baseline": {"value": r["value"], "unit": "voxels/s", "cores": r["cores"], "kind": "port",
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_06976_b200 as B
+    from oracle import bttb_oracle as O  # input recipe + cpu baseline only
+    from paper_1912_06976_b200.parallel import DeviceOperator, ShardedOperator, partition_layers
+
+    rank, world, local = dist_env()
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = a.config
+    desc, batch = workload(cfg, O)
+    og = O.config_grid(cfg)
+    kind, _ = O.config_kernel(cfg)
+    sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, dz, _, kargs, _ = O.CONFIGS[cfg]
+    grid = B.make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, og.z)
+    params = B.KernelParams.gravity() if kind == "gravity" else B.KernelParams.magnetic(*kargs)
+    lo, hi = partition_layers(nz, world)[rank]
+    np_dt = np.float64 if a.dtype == "f64" else np.float32
+    t_dt = torch.float64 if a.dtype == "f64" else torch.float32
+    bsz = 8 if a.dtype == "f64" else 4
+
+    def build(dtype):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = B.build_transform_stack(grid, params, dtype="float64" if dtype == "f64" else "float32",
+                                     device=local, layers=(lo, hi))
+        torch.cuda.synchronize()
+        return st, time.perf_counter() - t0
+
+    stack, t_build = build(a.dtype)
+    op = ShardedOperator(DeviceOperator(stack))
+    n_r = grid.n_r
+    # seeded inputs, generated on the host (the model slice of this rank), resident in HBM
+    rng = np.random.default_rng(1000 + rank)
+    if cfg in ("C4",):
+        xh = rng.uniform(0.0, 0.05, (batch, (hi - lo) * n_r))
+    elif cfg == "C5":
+        xh = rng.normal(0.0, 0.1, (batch, (hi - lo) * n_r))
+    else:
+        xh = rng.uniform(0.0, 1.0, (batch, (hi - lo) * n_r))
+    dh = np.random.default_rng(1).normal(0.0, 1.0, (batch, grid.m))
+    x_pin = torch.from_numpy(xh.astype(np_dt)).pin_memory()
+    d_pin = torch.from_numpy(dh.astype(np_dt)).pin_memory()
+    x = x_pin.to(dev)
+    d = d_pin.to(dev)
+    y = torch.empty((batch, grid.m), dtype=t_dt, device=dev)
+    xt = torch.empty((batch, (hi - lo) * n_r), dtype=t_dt, device=dev)
+    dwork = torch.empty_like(d)
+    xs = x if batch > 1 else x[0]
+    ys = y if batch > 1 else y[0]
+    ds = dwork if batch > 1 else dwork[0]
+    xts = xt if batch > 1 else xt[0]
+
+    def step():
+        op.forward(xs, ys)
+        ds.copy_(d if batch > 1 else d[0])
+        op.transpose(ds, xts)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    launches_per_apply = stack.info()[9]
+    # per-mode times (after the timed region; same stream, CUDA events)
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(reps):
+            fn()
+        s1.record(stream)
+        s1.synchronize()
+        return s0.elapsed_time(s1) / reps
+
+    reps = max(3, min(a.steps, 20))
+    fwd_ms = timed(lambda: DeviceOperator.forward(op.local, xs, ys), reps)
+    launch_fwd = stack.info()[9]
+    tra_ms = timed(lambda: DeviceOperator.transpose(op.local, ds, xts), reps)
+    launch_tra = stack.info()[9]
+
+    # end-to-end through the public C ABI with host (pinned) buffers
+    e2e = None
+    if not a.no_e2e:
+        yo = torch.empty((batch, grid.m), dtype=t_dt).pin_memory()
+        xo = torch.empty((batch, (hi - lo) * n_r), dtype=t_dt).pin_memory()
+        from paper_1912_06976_b200.multiply import apply_into
+
+        def e2e_step():
+            apply_into(stack, "forward", x_pin.data_ptr(), yo.data_ptr(), batch, host=True)
+            if world > 1:
+                t = yo.to(dev)
+                dist.all_reduce(t)
+                yo.copy_(t)
+            apply_into(stack, "transpose", d_pin.data_ptr(), xo.data_ptr(), batch, host=True)
+
+        e2e_step()
+        e_steps = max(2, min(a.steps, 10))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        barrier()
+        t_e2e = (time.perf_counter() - t0) / e_steps
+        if world > 1:
+            tt = torch.tensor([t_e2e], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": batch * grid.n / t_e2e, "unit": "voxels/s",
+               "h2d_bytes_per_step": int(x_pin.numel() * bsz + d_pin.numel() * bsz),
+               "d2h_bytes_per_step": int(yo.numel() * bsz + xo.numel() * bsz),
+               "ms_per_step": 1e3 * t_e2e}
+
+    # max over ranks
+    vals = torch.tensor([ms, fwd_ms, tra_ms, t_build], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, fwd_ms, tra_ms, t_build = vals.tolist()
+
+    variants = {}
+    if not a.no_variants and cfg == "C4":
+        other = "f32" if a.dtype == "f64" else "f64"
+        st2, tb2 = build(other)
+        op2 = DeviceOperator(st2)
+        o_dt = torch.float32 if other == "f32" else torch.float64
+        x2, d2 = xs.to(o_dt), ds.to(o_dt)
+        y2 = torch.empty_like(ys, dtype=o_dt)
+        xt2 = torch.empty_like(xts, dtype=o_dt)
+
+        def step2():
+            op2.forward(x2, y2)
+            if world > 1:
+                dist.all_reduce(y2)
+                dist.broadcast(d2, 0)
+            op2.transpose(d2, xt2)
+
+        for _ in range(3):
+            step2()
+        barrier()
+        r2 = max(3, min(a.steps, 50))
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(r2):
+            step2()
+        s1.record(stream)
+        barrier()
+        ms2 = s0.elapsed_time(s1) / r2
+        b2 = 8 if other == "f64" else 4
+        peak, _ = peaks()
+        variants[other] = {"ms_per_step": ms2, "value": batch * grid.n / (ms2 * 1e-3),
+                           "roofline_frac": 2 * algorithmic_bytes(og, b2, batch) / (ms2 * 1e-3) / 1e9 / peak,
+                           "build_s": tb2}
+        st2.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = peaks()
+    B_apply = algorithmic_bytes(og, bsz, batch)
+    achieved = 2 * B_apply / (ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                traffic = json.load(fh).get(f"{cfg}_{a.dtype}")
+        except (OSError, ValueError):
+            traffic = None
+    cpu = None
+    if not a.no_cpu_baseline and world == 1:
+        cores = os.cpu_count() or 1
+        cpu = cpu_sample(cfg, 1, 1, min(nz, cores) if cfg in ("C4", "C5") else None)
+    line = {
+        "metric": METRIC,
+        "value": batch * grid.n / (ms * 1e-3),
+        "unit": "voxels/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": max(3, a.warmup),
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": a.dtype,
+        "data": "synthetic, seeded host-generated inputs resident in HBM (no dataset exists; SURVEY.md 8(d))",
+        "config": {"workload": desc, "fft_shape": list(stack.fft_shape),
+                   "layers_per_rank": hi - lo, "parallelism": f"layer-shard x{world}",
+                   "l2": "inputs larger than L2 (spectra %.2f GB + model %.2f GB per rank)" % (
+                       stack.device_bytes / 1e9,
+                       x.numel() * bsz / 1e9),
+                   "step": "1 forward (+all-reduce) + 1 transpose (+broadcast)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "frac_of_8TBs_nameplate": achieved / 8000.0,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_apply": B_apply,
+                     "kernel": "fused operator (row R2C -> column FFT*S accumulate -> column IFFT -> row C2R)"},
+        "fwd_ms": fwd_ms, "tra_ms": tra_ms, "build_s": t_build,
+        "fwd_voxels_per_s": batch * grid.n / (fwd_ms * 1e-3),
+        "tra_voxels_per_s": batch * grid.n / (tra_ms * 1e-3),
+        "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "sample")}
+        | {"kind": "port"},
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": int((launch_fwd + launch_tra) * a.steps),
+        "launches_per_step": int(launch_fwd + launch_tra),
+        "variants": variants,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -347,3 +347,27 @@ def make_inputs(name, g=None, seed_model=0, seed_data=1, batch=None):
         raise KeyError(name)
     d = rd.normal(0.0, 1.0, (b, g.m))
     return x, d
+
+
+# --------------------------------------------------------------------------
+# threaded layer loop (bench.py CPU arm).  numpy's pocketfft releases the GIL,
+# so layers run concurrently; per-layer results are combined in layer order,
+# giving exactly the serial loop's numbers.
+# --------------------------------------------------------------------------
+def build_spectra_threaded(g, kind, consts, layers, pool):
+    pairs = list(pool.map(lambda r: build_spectra(g, kind, consts, [r]), layers))
+    return [p[0][0] for p in pairs], [p[1][0] for p in pairs]
+
+
+def forward_threaded(g, fw, x, pool):
+    parts = list(pool.map(
+        lambda k: forward(g, [fw[k]], x[k * g.n_r:(k + 1) * g.n_r], layers=[k]), range(len(fw))))
+    d = np.zeros(g.m)
+    for p in parts:
+        d += p
+    return d
+
+
+def transpose_threaded(g, tr, v, pool):
+    parts = list(pool.map(lambda T: transpose(g, [T], v), tr))
+    return np.concatenate(parts)

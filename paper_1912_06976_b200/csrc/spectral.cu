@@ -286,14 +286,22 @@ int cols_per_cta(int nt, int L, int Hx) {
     default: return cudaErrorInvalidValue;             \
   }
 
+template <class K>
+int team_limit(K kern, int nt) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
+  return fa.maxThreadsPerBlock / nt > 0 ? fa.maxThreadsPerBlock / nt : 1;
+}
+
 template <class T>
 cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
-  const int P = pairs_per_cta<T>(d.nt, d.L, a.nrows);
-  const size_t smem = (size_t)P * team_stride(d.L) * sizeof(cplx<T>);
-  dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * d.nt);
   BTTB_E_DISPATCH(E, {
     auto kern = k_row_r2c<T, EE>;
+    int P = pairs_per_cta<T>(d.nt, d.L, a.nrows);
+    P = P < team_limit(kern, d.nt) ? P : team_limit(kern, d.nt);
+    const size_t smem = (size_t)P * team_stride(d.L) * sizeof(cplx<T>);
+    dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * d.nt);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<grd, blk, smem, st>>>(a, d, P);
@@ -304,11 +312,12 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
 template <class T>
 cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
-  const int P = pairs_per_cta<T>(d.nt, d.L, a.nrows);
-  const size_t smem = (size_t)P * team_stride(d.L) * sizeof(cplx<T>);
-  dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * d.nt);
   BTTB_E_DISPATCH(E, {
     auto kern = k_row_c2r<T, EE>;
+    int P = pairs_per_cta<T>(d.nt, d.L, a.nrows);
+    P = P < team_limit(kern, d.nt) ? P : team_limit(kern, d.nt);
+    const size_t smem = (size_t)P * team_stride(d.L) * sizeof(cplx<T>);
+    dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * d.nt);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<grd, blk, smem, st>>>(a, d, P);
@@ -319,11 +328,12 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
 template <class T>
 cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
-  const int C = cols_per_cta<T>(d.nt, d.L, a.Hx);
-  const size_t smem = (size_t)C * team_stride(d.L) * sizeof(cplx<T>);
-  dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * d.nt);
   BTTB_E_DISPATCH(E, {
     auto kern = k_col_fwd<T, EE>;
+    int C = cols_per_cta<T>(d.nt, d.L, a.Hx);
+    C = C < team_limit(kern, d.nt) ? C : team_limit(kern, d.nt);
+    const size_t smem = (size_t)C * team_stride(d.L) * sizeof(cplx<T>);
+    dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * d.nt);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<grd, blk, smem, st>>>(a, d, C);
@@ -334,11 +344,12 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
 template <class T>
 cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
-  const int C = cols_per_cta<T>(d.nt, d.L, a.Hx);
-  const size_t smem = (size_t)C * team_stride(d.L) * sizeof(cplx<T>);
-  dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * d.nt);
   BTTB_E_DISPATCH(E, {
     auto kern = k_col_tra<T, EE>;
+    int C = cols_per_cta<T>(d.nt, d.L, a.Hx);
+    C = C < team_limit(kern, d.nt) ? C : team_limit(kern, d.nt);
+    const size_t smem = (size_t)C * team_stride(d.L) * sizeof(cplx<T>);
+    dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * d.nt);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<grd, blk, smem, st>>>(a, d, C);
@@ -348,11 +359,12 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
 
 template <class TS>
 cudaError_t launch_col_spec(const ColSpecArgs& a, const FFTDesc<double>& d, int E, cudaStream_t st) {
-  const int C = cols_per_cta<double>(d.nt, d.L, a.Hx);
-  const size_t smem = (size_t)C * team_stride(d.L) * sizeof(double2);
-  dim3 grd((a.Hx + C - 1) / C), blk(C * d.nt);
   BTTB_E_DISPATCH(E, {
     auto kern = k_col_spec<TS, EE>;
+    int C = cols_per_cta<double>(d.nt, d.L, a.Hx);
+    C = C < team_limit(kern, d.nt) ? C : team_limit(kern, d.nt);
+    const size_t smem = (size_t)C * team_stride(d.L) * sizeof(double2);
+    dim3 grd((a.Hx + C - 1) / C), blk(C * d.nt);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<grd, blk, smem, st>>>(a, d, C);
