@@ -64,19 +64,17 @@ int64_t pick_length(int64_t n) {
   return -1;
 }
 
-struct FFTPlanHost {
-  int L = 0, E = 0, nt = 0, npass = 0;
+// Radix plan of one length at one precision: E elements per thread
+// (fp64 keeps E small for register pressure: 8 / 12 / 10; fp32: 8 / 12 / 20).
+struct RadixPlan {
+  int E = 0, nt = 0, npass = 0;
   int radix[8] = {0};
-  double2* tw64 = nullptr;
-  float2* tw32 = nullptr;
-
-  int init(int64_t len) {
-    L = (int)len;
-    E = length_family(len);
-    if (!E) return fail(BTTB_EINVAL, "unsupported FFT length %lld", (long long)len);
+  int init(int L, int fam, bool fp64) {
+    E = fam == 20 && fp64 ? 10 : fam;
     nt = L / E;
-    static const int cand8[] = {8, 4, 2, 0}, cand12[] = {12, 6, 4, 3, 2, 0}, cand20[] = {20, 10, 5, 4, 2, 0};
-    const int* cand = E == 8 ? cand8 : E == 12 ? cand12 : cand20;
+    static const int c8[] = {8, 4, 2, 0}, c12[] = {12, 6, 4, 3, 2, 0}, c20[] = {20, 10, 5, 4, 2, 0},
+                     c10[] = {10, 5, 2, 0};
+    const int* cand = E == 8 ? c8 : E == 12 ? c12 : E == 20 ? c20 : c10;
     int rem = L;
     npass = 0;
     while (rem > 1) {
@@ -87,6 +85,27 @@ struct FFTPlanHost {
       radix[npass++] = r;
       rem /= r;
     }
+    return BTTB_OK;
+  }
+  unsigned code() const {
+    unsigned c = 0;
+    for (int i = 0; i < npass; ++i) c |= radix_code(radix[i]) << (4 * i);
+    return c;
+  }
+};
+
+struct FFTPlanHost {
+  int L = 0;
+  RadixPlan p64, p32;
+  double2* tw64 = nullptr;
+  float2* tw32 = nullptr;
+
+  int init(int64_t len) {
+    L = (int)len;
+    const int fam = length_family(len);
+    if (!fam) return fail(BTTB_EINVAL, "unsupported FFT length %lld", (long long)len);
+    int rc;
+    if ((rc = p64.init(L, fam, true)) || (rc = p32.init(L, fam, false))) return rc;
     std::vector<double2> h64(L);
     std::vector<float2> h32(L);
     for (int m = 0; m < L; ++m) {
@@ -108,14 +127,18 @@ struct FFTPlanHost {
     tw64 = nullptr;
     tw32 = nullptr;
   }
+  template <class T> const RadixPlan& plan() const {
+    if constexpr (std::is_same<T, double>::value) return p64; else return p32;
+  }
+  template <class T> int E() const { return plan<T>().E; }
   template <class T> FFTDesc<T> desc() const {
     FFTDesc<T> d;
     if constexpr (std::is_same<T, double>::value) d.tw = tw64; else d.tw = tw32;
+    const RadixPlan& rp = plan<T>();
     d.L = L;
-    d.nt = nt;
-    d.npass = npass;
-    d.code = 0;
-    for (int i = 0; i < npass; ++i) d.code |= radix_code(radix[i]) << (4 * i);
+    d.nt = rp.nt;
+    d.npass = rp.npass;
+    d.code = rp.code();
     return d;
   }
 };
@@ -156,7 +179,7 @@ struct DeviceGuard {
 size_t chunk_budget() {
   const char* env = getenv("BTTB_CHUNK_BYTES");
   if (env) return (size_t)atoll(env);
-  return (size_t)48 << 20;
+  return (size_t)64 << 20;
 }
 
 }  // namespace
@@ -307,7 +330,7 @@ int build_spectra(bttb_plan_s* p) {
     ra.out_sstride = 0;
     ra.ld_out = (int)p->Ly;
     ra.Hx = (int)p->Hx;
-    e = launch_row_r2c<double>(ra, dx, p->fx.E, st);
+    e = launch_row_r2c<double>(ra, dx, p->fx.E<double>(), st);
     if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "build row pass: %s", cudaGetErrorString(e)); break; }
     ColSpecArgs ca{};
     ca.Y = yb.p;
@@ -316,8 +339,8 @@ int build_spectra(bttb_plan_s* p) {
     ca.lds = (int)p->Ly;
     ca.Hx = (int)p->Hx;
     ca.scale = scale;
-    e = p->dtype == BTTB_F64 ? launch_col_spec<double>(ca, dy, p->fy.E, st)
-                             : launch_col_spec<float>(ca, dy, p->fy.E, st);
+    e = p->dtype == BTTB_F64 ? launch_col_spec<double>(ca, dy, p->fy.E<double>(), st)
+                             : launch_col_spec<float>(ca, dy, p->fy.E<double>(), st);
     if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "build column pass: %s", cudaGetErrorString(e)); break; }
   }
   if (!rc) {
@@ -371,7 +394,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ra.out_sstride = (long long)Hx * ny;
         ra.ld_out = (int)ny;
         ra.Hx = (int)Hx;
-        CU(launch_row_r2c<T>(ra, dx, p->fx.E, st));
+        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
         ColFwdArgs ca{};
         ca.Y = Yb;
         ca.y_bstride = (long long)k * Hx * ny;
@@ -389,7 +412,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.accumulate = r0 > 0;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
-        CU(launch_col_fwd<T>(ca, dy, p->fy.E, st));
+        CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), st));
         launches += 2;
       }
       RowC2RArgs oa{};
@@ -405,7 +428,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       oa.spb = 1;
       oa.ld_out = (int)sx;
       oa.nout = (int)sx;
-      CU(launch_row_c2r<T>(oa, dx, p->fx.E, st));
+      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
       launches += 1;
     } else {
       RowR2CArgs ra{};
@@ -421,7 +444,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       ra.out_sstride = (long long)Hx * sy;
       ra.ld_out = (int)sy;
       ra.Hx = (int)Hx;
-      CU(launch_row_r2c<T>(ra, dx, p->fx.E, st));
+      CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
       launches += 1;
       T* yout = static_cast<T*>(y) + b0 * nloc;
       for (int64_t r0 = 0; r0 < p->nzl; r0 += K) {
@@ -442,7 +465,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.nout = (int)ny;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
-        CU(launch_col_tra<T>(ca, dy, p->fy.E, st));
+        CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), st));
         RowC2RArgs oa{};
         oa.in = Yb;
         oa.in_sstride = (long long)Hx * ny;
@@ -456,7 +479,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         oa.spb = k;
         oa.ld_out = (int)nx;
         oa.nout = (int)nx;
-        CU(launch_row_c2r<T>(oa, dx, p->fx.E, st));
+        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
         launches += 2;
       }
     }

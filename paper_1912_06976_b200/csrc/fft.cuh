@@ -149,6 +149,18 @@ __device__ __forceinline__ void dft(V* x) {
   }
 }
 
+// Shared-memory slot of element i of a team buffer: one pad slot after every
+// 8 (fp64) / 16 (fp32) elements, so the strided Stockham scatters spread over
+// the 32 banks.  team_slots(L) is the padded size of one team buffer (+1 slot
+// staggers consecutive teams).
+template <class T> __host__ __device__ __forceinline__ int pslot(int i) {
+  return i + (i >> (sizeof(T) == 8 ? 3 : 4));
+}
+template <class T> __host__ __device__ __forceinline__ int team_slots(int L) { return pslot<T>(L) + 1; }
+// plan-specific padding e + e / PAD (PAD chosen per plan by a bank-conflict search
+// over all of the plan's exchange patterns, tools/bank_search.py)
+template <int PAD> __host__ __device__ __forceinline__ int pad_slot(int i) { return i + i / PAD; }
+
 // Plan for one transform length, passed by value to kernels.
 template <class T>
 struct FFTDesc {
@@ -208,7 +220,7 @@ __device__ __forceinline__ void pass_store(const cplx<T> (&v)[E], cplx<T>* sm, i
     const int j = t + nt * b;
     const int k = j % Ns;
     const int base = (j - k) * R + k;
-    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; sm[base + r * Ns] = v[b + r * NB]; });
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; sm[pslot<T>(base + r * Ns)] = v[b + r * NB]; });
   });
 }
 
@@ -262,10 +274,97 @@ __device__ __forceinline__ void team_fft(cplx<T> (&v)[E], cplx<T>* sm, int t, co
       run_store<T, E>(R, v, sm, t, d.nt, Ns);
       __syncthreads();
 #pragma unroll
-      for (int s = 0; s < E; ++s) v[s] = sm[t + d.nt * s];
+      for (int s = 0; s < E; ++s) v[s] = sm[pslot<T>(t + d.nt * s)];
     }
     Ns *= R;
   }
 }
+
+// ---------------------------------------------------------------------------
+// Compile-time radix plans for the hot lengths: the pass sequence, Ns, the
+// twiddle stride and the team size are constants, so the index arithmetic
+// folds (no runtime integer division) and every pass is fully unrolled.
+// ---------------------------------------------------------------------------
+template <class T, int E, int R, int NS, int NT, int L>
+__device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw) {
+  using V = cplx<T>;
+  constexpr int NB = E / R;
+  constexpr int STRIDE = L / (NS * R);
+  sfor<0, NB>([&](auto bc) {
+    constexpr int b = decltype(bc)::value;
+    V u[R];
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; u[r] = v[b + r * NB]; });
+    if constexpr (NS > 1) {
+      const int k = (t + NT * b) % NS;
+      sfor<1, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        u[r] = cmul(u[r], __ldg(&tw[r * STRIDE * k]));
+      });
+    }
+    dft<R>(u);
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; v[b + r * NB] = u[r]; });
+  });
+}
+
+template <class T, int E, int R, int NS, int NT, int PAD>
+__device__ __forceinline__ void spass_store(const cplx<T> (&v)[E], cplx<T>* sm, int t) {
+  constexpr int NB = E / R;
+  sfor<0, NB>([&](auto bc) {
+    constexpr int b = decltype(bc)::value;
+    const int j = t + NT * b;
+    const int k = j % NS;
+    const int base = (j - k) * R + k;
+    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; sm[pad_slot<PAD>(base + r * NS)] = v[b + r * NB]; });
+  });
+}
+
+template <class T, int E, int L, int PAD, int NS, int R, int... Rest>
+__device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw) {
+  constexpr int NT = L / E;
+  static_assert(E % R == 0, "radix must divide elements per thread");
+  spass_compute<T, E, R, NS, NT, L>(v, t, tw);
+  if constexpr (sizeof...(Rest) > 0) {
+    __syncthreads();
+    spass_store<T, E, R, NS, NT, PAD>(v, sm, t);
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < E; ++s) v[s] = sm[pad_slot<PAD>(t + NT * s)];
+    sfft<T, E, L, PAD, NS * R, Rest...>(v, sm, t, tw);
+  }
+}
+
+// Plan concepts used by the kernels: Scalar, E, nt(d), slot(e), slots(L),
+// fft(v, sm, t, d); kStatic / NT for launch bounds.
+template <class T, int E_, int PAD, int... Rs>
+struct SPlan {
+  using Scalar = T;
+  static constexpr bool kStatic = true;
+  static constexpr int E = E_;
+  static constexpr int L = (Rs * ...);
+  static constexpr int NT = L / E_;
+  static_assert(L % E_ == 0, "E must divide L");
+  __host__ __device__ __forceinline__ static int nt(const FFTDesc<T>&) { return NT; }
+  __host__ __device__ __forceinline__ static int slot(int e) { return pad_slot<PAD>(e); }
+  __host__ __device__ __forceinline__ static int slots(int len) { return pad_slot<PAD>(len) + 1; }
+  __device__ __forceinline__ static void fft(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d) {
+    sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw);
+  }
+};
+
+// Runtime-radix plan; MAXT bounds the CTA size (256 keeps registers free for
+// the common small lengths, 1024 is for teams of more than 256 threads).
+template <class T, int E_, int MAXT = 256>
+struct DPlan {
+  using Scalar = T;
+  static constexpr bool kStatic = false;
+  static constexpr int E = E_;
+  static constexpr int NT = MAXT;
+  __host__ __device__ __forceinline__ static int nt(const FFTDesc<T>& d) { return d.nt; }
+  __host__ __device__ __forceinline__ static int slot(int e) { return pslot<T>(e); }
+  __host__ __device__ __forceinline__ static int slots(int len) { return team_slots<T>(len); }
+  __device__ __forceinline__ static void fft(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d) {
+    team_fft<T, E_>(v, sm, t, d);
+  }
+};
 
 }  // namespace bttb

@@ -9,21 +9,23 @@
 //  * forward: spectra of a chunk of layers are summed before ONE inverse
 //    column FFT per chunk (multiply.py:42-45 does one per layer);
 //  * transpose spectrum = conj(forward spectrum) (transform.py:75-82,102).
+//
+// Memory hints: the cached spectra and the model vectors are streamed exactly
+// once per application, so they are loaded with evict-first (ld.global.cs)
+// and the transpose's model output is stored with st.global.cs; the chunk
+// intermediates (row-pass output Y, accumulator W) use the default policy so
+// they stay L2-resident between the row and column kernels.
 #include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "spectral.h"
 
 namespace bttb {
 
 namespace {
-
-constexpr int kMaxThreads = 1024;
-
-template <class T> struct Prec;
-template <> struct Prec<double> { static constexpr int pairs = 4; static constexpr int cols_threads = 256; };
-template <> struct Prec<float> { static constexpr int pairs = 8; static constexpr int cols_threads = 256; };
-
-__host__ __device__ inline int team_stride(int L) { return L + 1; }  // +1 element staggers teams across banks
 
 template <class K>
 cudaError_t set_smem(K kernel, size_t bytes) {
@@ -36,19 +38,21 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 // ---------------------------------------------------------------------------
 // Row pass, real -> half spectrum, two rows per complex FFT
 // ---------------------------------------------------------------------------
-template <class T, int E>
-__global__ void k_row_r2c(RowR2CArgs a, FFTDesc<T> d, int P) {
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_row_r2c(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, int P) {
+  using T = typename PL::Scalar;
   using V = cplx<T>;
+  constexpr int E = PL::E;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* smb = reinterpret_cast<V*>(smraw);
-  const int L = d.L, nt = d.nt, Ls = team_stride(L);
+  const int L = d.L, nt = PL::nt(d), Ls = PL::slots(L);
   const int tid = threadIdx.x, c = tid / nt, t = tid - c * nt;
   const int s = blockIdx.y;
   const int q0 = blockIdx.x * 2 * P;
   const int qa = q0 + 2 * c, qb = qa + 1;
   const T* in = static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride +
                 (long long)(s % a.spb) * a.in_sstride;
-  const bool va = (c < P) && qa < a.nrows, vb = (c < P) && qb < a.nrows;
+  const bool va = qa < a.nrows, vb = qb < a.nrows;
   const T* ra = in + (long long)(va ? qa : 0) * a.ld_in;
   const T* rb = in + (long long)(vb ? qb : 0) * a.ld_in;
   V v[E];
@@ -56,13 +60,13 @@ __global__ void k_row_r2c(RowR2CArgs a, FFTDesc<T> d, int P) {
   for (int k = 0; k < E; ++k) {
     const int i = t + nt * k;
     const bool inb = i < a.nvalid;
-    v[k] = mkc<V>(va && inb ? ra[i] : T(0), vb && inb ? rb[i] : T(0));
+    v[k] = mkc<V>(va && inb ? __ldcs(ra + i) : T(0), vb && inb ? __ldcs(rb + i) : T(0));
   }
   V* sm = smb + (long long)c * Ls;
-  team_fft<T, E>(v, sm, t, d);
+  PL::fft(v, sm, t, d);
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < E; ++k) sm[t + nt * k] = v[k];
+  for (int k = 0; k < E; ++k) sm[PL::slot(t + nt * k)] = v[k];
   __syncthreads();
   // separate the two real transforms and store transposed: out[s][kx][q]
   V* out = static_cast<V*>(a.out) + (long long)s * a.out_sstride;
@@ -71,8 +75,8 @@ __global__ void k_row_r2c(RowR2CArgs a, FFTDesc<T> d, int P) {
     const int kx = it / P, cc = it - kx * P;
     const int q = q0 + 2 * cc;
     const V* z = smb + (long long)cc * Ls;
-    const V zk = z[kx];
-    const V zm = z[kx == 0 ? 0 : L - kx];
+    const V zk = z[PL::slot(kx)];
+    const V zm = z[PL::slot(kx == 0 ? 0 : L - kx)];
     const T h = T(0.5);
     V* o = out + (long long)kx * a.ld_out + q;
     if (q < a.nrows) o[0] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
@@ -83,12 +87,14 @@ __global__ void k_row_r2c(RowR2CArgs a, FFTDesc<T> d, int P) {
 // ---------------------------------------------------------------------------
 // Row pass, half spectrum -> real rows (two rows per complex inverse FFT)
 // ---------------------------------------------------------------------------
-template <class T, int E>
-__global__ void k_row_c2r(RowC2RArgs a, FFTDesc<T> d, int P) {
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_row_c2r(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, int P) {
+  using T = typename PL::Scalar;
   using V = cplx<T>;
+  constexpr int E = PL::E;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* smb = reinterpret_cast<V*>(smraw);
-  const int L = d.L, nt = d.nt, Ls = team_stride(L);
+  const int L = d.L, nt = PL::nt(d), Ls = PL::slots(L);
   const int tid = threadIdx.x, c = tid / nt, t = tid - c * nt;
   const int s = blockIdx.y;
   const int j0 = blockIdx.x * 2 * P;
@@ -105,17 +111,17 @@ __global__ void k_row_c2r(RowC2RArgs a, FFTDesc<T> d, int P) {
       B.y = T(0);
     }
     V* z = smb + (long long)cc * Ls;
-    z[kx] = mkc<V>(A.x - B.y, A.y + B.x);
-    if (kx >= 1 && kx <= L - a.Hx) z[L - kx] = mkc<V>(A.x + B.y, B.x - A.y);
+    z[PL::slot(kx)] = mkc<V>(A.x - B.y, A.y + B.x);
+    if (kx >= 1 && kx <= L - a.Hx) z[PL::slot(L - kx)] = mkc<V>(A.x + B.y, B.x - A.y);
   }
   __syncthreads();
   V* sm = smb + (long long)c * Ls;
   V v[E];
 #pragma unroll
-  for (int k = 0; k < E; ++k) v[k] = conjv(sm[t + nt * k]);
-  team_fft<T, E>(v, sm, t, d);
+  for (int k = 0; k < E; ++k) v[k] = conjv(sm[PL::slot(t + nt * k)]);
+  PL::fft(v, sm, t, d);
   const int ja = j0 + 2 * c, jb = ja + 1;
-  const bool va = (c < P) && ja < a.nrows, vb = (c < P) && jb < a.nrows;
+  const bool va = ja < a.nrows, vb = jb < a.nrows;
   T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
   T* oa = out + (long long)(va ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : 0) * a.ld_out;
@@ -123,8 +129,8 @@ __global__ void k_row_c2r(RowC2RArgs a, FFTDesc<T> d, int P) {
   for (int k = 0; k < E; ++k) {
     const int i = t + nt * k;
     if (i < a.nout) {
-      if (va) oa[i] = v[k].x;
-      if (vb) ob[i] = -v[k].y;
+      if (va) __stcs(oa + i, v[k].x);
+      if (vb) __stcs(ob + i, -v[k].y);
     }
   }
 }
@@ -133,14 +139,16 @@ __global__ void k_row_c2r(RowC2RArgs a, FFTDesc<T> d, int P) {
 // Forward column stage: FFT along y, multiply by cached spectrum, accumulate
 // over the chunk's layers in registers, one inverse FFT, extract stations.
 // ---------------------------------------------------------------------------
-template <class T, int E>
-__global__ void k_col_fwd(ColFwdArgs a, FFTDesc<T> d, int C) {
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_fwd(ColFwdArgs a, FFTDesc<typename PL::Scalar> d, int C) {
+  using T = typename PL::Scalar;
   using V = cplx<T>;
+  constexpr int E = PL::E;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int L = d.L, nt = d.nt, Ls = team_stride(L);
+  const int nt = PL::nt(d), Ls = PL::slots(d.L);
   const int tid = threadIdx.x, c = tid / nt, t = tid - c * nt;
   const int kx = blockIdx.x * C + c;
-  const bool kv = (c < C) && kx < a.Hx;
+  const bool kv = kx < a.Hx;
   const int kxc = kv ? kx : 0;
   const int b = blockIdx.y;
   V* sm = reinterpret_cast<V*>(smraw) + (long long)c * Ls;
@@ -156,18 +164,18 @@ __global__ void k_col_fwd(ColFwdArgs a, FFTDesc<T> d, int C) {
       const int q = t + nt * k;
       v[k] = q < a.nvalid ? yc[q] : mkc<V>(T(0), T(0));
     }
-    team_fft<T, E>(v, sm, t, d);
+    PL::fft(v, sm, t, d);
     const V* sc = Sb + (long long)r * a.s_rstride;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      const V w = __ldg(&sc[t + nt * k]);
+      const V w = __ldcs(sc + t + nt * k);
       acc[k].x += w.x * v[k].x - w.y * v[k].y;
       acc[k].y += w.x * v[k].y + w.y * v[k].x;
     }
   }
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
-  team_fft<T, E>(acc, sm, t, d);
+  PL::fft(acc, sm, t, d);
   if (kv) {
     V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
 #pragma unroll
@@ -186,14 +194,16 @@ __global__ void k_col_fwd(ColFwdArgs a, FFTDesc<T> d, int C) {
 // Transpose column stage: FFT of the data column once, then per layer
 // conj(spectrum) multiply and inverse FFT, extract prism rows.
 // ---------------------------------------------------------------------------
-template <class T, int E>
-__global__ void k_col_tra(ColTraArgs a, FFTDesc<T> d, int C) {
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<typename PL::Scalar> d, int C) {
+  using T = typename PL::Scalar;
   using V = cplx<T>;
+  constexpr int E = PL::E;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int L = d.L, nt = d.nt, Ls = team_stride(L);
+  const int nt = PL::nt(d), Ls = PL::slots(d.L);
   const int tid = threadIdx.x, c = tid / nt, t = tid - c * nt;
   const int kx = blockIdx.x * C + c;
-  const bool kv = (c < C) && kx < a.Hx;
+  const bool kv = kx < a.Hx;
   const int kxc = kv ? kx : 0;
   const int b = blockIdx.y;
   V* sm = reinterpret_cast<V*>(smraw) + (long long)c * Ls;
@@ -204,7 +214,7 @@ __global__ void k_col_tra(ColTraArgs a, FFTDesc<T> d, int C) {
     const int j = t + nt * k;
     dh[k] = j < a.nvalid ? dc[j] : mkc<V>(T(0), T(0));
   }
-  team_fft<T, E>(dh, sm, t, d);
+  PL::fft(dh, sm, t, d);
   const V* Sb = static_cast<const V*>(a.S) + (long long)kxc * a.lds;
   V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kxc * a.ldw;
   for (int r = 0; r < a.K; ++r) {
@@ -212,10 +222,10 @@ __global__ void k_col_tra(ColTraArgs a, FFTDesc<T> d, int C) {
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       // conj(conj(S) * dh) = S * conj(dh): inverse FFT via the conjugation identity
-      const V w = __ldg(&sc[t + nt * k]);
+      const V w = __ldcs(sc + t + nt * k);
       v[k] = mkc<V>(w.x * dh[k].x + w.y * dh[k].y, w.y * dh[k].x - w.x * dh[k].y);
     }
-    team_fft<T, E>(v, sm, t, d);
+    PL::fft(v, sm, t, d);
     if (kv) {
       V* wc = Wb + (long long)r * a.w_rstride;
 #pragma unroll
@@ -230,22 +240,23 @@ __global__ void k_col_tra(ColTraArgs a, FFTDesc<T> d, int C) {
 // ---------------------------------------------------------------------------
 // Spectrum build, column stage (fp64 FFT, stored as TS, scaled)
 // ---------------------------------------------------------------------------
-template <class TS, int E>
-__global__ void k_col_spec(ColSpecArgs a, FFTDesc<double> d, int C) {
+template <class PL, class TS, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_spec(ColSpecArgs a, FFTDesc<double> d, int C) {
   using V = double2;
   using VS = cplx<TS>;
+  constexpr int E = PL::E;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int L = d.L, nt = d.nt, Ls = team_stride(L);
+  const int nt = PL::nt(d), Ls = PL::slots(d.L);
   const int tid = threadIdx.x, c = tid / nt, t = tid - c * nt;
   const int kx = blockIdx.x * C + c;
-  const bool kv = (c < C) && kx < a.Hx;
+  const bool kv = kx < a.Hx;
   const int kxc = kv ? kx : 0;
   V* sm = reinterpret_cast<V*>(smraw) + (long long)c * Ls;
   V v[E];
   const V* yc = static_cast<const V*>(a.Y) + (long long)kxc * a.ldy;
 #pragma unroll
   for (int k = 0; k < E; ++k) v[k] = yc[t + nt * k];
-  team_fft<double, E>(v, sm, t, d);
+  PL::fft(v, sm, t, d);
   if (kv) {
     VS* sc = static_cast<VS*>(a.S) + (long long)kx * a.lds;
 #pragma unroll
@@ -254,122 +265,203 @@ __global__ void k_col_spec(ColSpecArgs a, FFTDesc<double> d, int C) {
 }
 
 // ---------------------------------------------------------------------------
-// launchers
+// plan registry: compile-time plans for the BASELINE lengths (PAD from
+// tools/bank_search.py), runtime-radix plans for every other supported length
 // ---------------------------------------------------------------------------
-namespace {
+template <class P> struct Tag { using type = P; };
 
-template <class T>
-int pairs_per_cta(int nt, int L, int nrows) {
-  int P = Prec<T>::pairs;
-  while (P > 1 && (P * nt > kMaxThreads || (size_t)P * team_stride(L) * sizeof(cplx<T>) > 200 * 1024)) P /= 2;
-  // small transforms: more teams per CTA
-  while (P * nt < 128 && 2 * P * team_stride(L) * sizeof(cplx<T>) <= 96 * 1024 && 2 * P <= (nrows + 1) / 2 + 1) P *= 2;
+template <class T, class F>
+cudaError_t with_plan(int L, int E, F&& f) {
+  if constexpr (sizeof(T) == 8) {
+    switch (L) {
+      case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
+      case 512: return f(Tag<SPlan<double, 8, 8, 8, 8, 8>>{});
+      case 432: return f(Tag<SPlan<double, 12, 12, 12, 12, 3>>{});
+      case 384: return f(Tag<SPlan<double, 12, 24, 12, 4, 4, 2>>{});
+      case 100: return f(Tag<SPlan<double, 20, 12, 20, 5>>{});
+      case 80: return f(Tag<SPlan<double, 20, 10, 20, 4>>{});
+      default: break;
+    }
+    const bool big = L / E > 256;
+    switch (E) {
+      case 8: return big ? f(Tag<DPlan<double, 8, 1024>>{}) : f(Tag<DPlan<double, 8, 256>>{});
+      case 12: return big ? f(Tag<DPlan<double, 12, 1024>>{}) : f(Tag<DPlan<double, 12, 256>>{});
+      case 10: return big ? f(Tag<DPlan<double, 10, 1024>>{}) : f(Tag<DPlan<double, 10, 256>>{});
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (L) {
+      case 2000: return f(Tag<SPlan<float, 20, 80, 20, 20, 5>>{});
+      case 512: return f(Tag<SPlan<float, 8, 16, 8, 8, 8>>{});
+      case 432: return f(Tag<SPlan<float, 12, 36, 12, 12, 3>>{});
+      case 384: return f(Tag<SPlan<float, 12, 48, 12, 4, 4, 2>>{});
+      case 100: return f(Tag<SPlan<float, 20, 10, 20, 5>>{});
+      case 80: return f(Tag<SPlan<float, 20, 10, 20, 4>>{});
+      default: break;
+    }
+    const bool big = L / E > 256;
+    switch (E) {
+      case 8: return big ? f(Tag<DPlan<float, 8, 1024>>{}) : f(Tag<DPlan<float, 8, 256>>{});
+      case 12: return big ? f(Tag<DPlan<float, 12, 1024>>{}) : f(Tag<DPlan<float, 12, 256>>{});
+      case 20: return big ? f(Tag<DPlan<float, 20, 1024>>{}) : f(Tag<DPlan<float, 20, 256>>{});
+      default: return cudaErrorInvalidValue;
+    }
+  }
+}
+
+// Fixed launch shapes of the compile-time plans: teams per CTA and the
+// register target that sets __launch_bounds__ min-blocks (fp64 column kernels
+// keep an E-element accumulator, hence the larger budget).
+template <class PL> struct Shape {
+  using T = typename PL::Scalar;
+  static constexpr int NT = PL::NT;
+  static constexpr int row_pairs = PL::kStatic ? (128 / (2 * NT) > (sizeof(T) == 8 ? 1 : 2) ? 128 / (2 * NT) : (sizeof(T) == 8 ? 1 : 2)) : 0;
+  static constexpr int col_teams = PL::kStatic ? (128 / NT > 1 ? 128 / NT : 1) : 0;
+  static constexpr int row_threads = PL::kStatic ? row_pairs * NT : NT;
+  static constexpr int col_threads = PL::kStatic ? col_teams * NT : NT;
+  static constexpr int warps(int threads) { return (threads + 31) / 32; }
+  static constexpr int minb(int threads, int regs) {
+    return 2048 / (warps(threads) * regs) > 1 ? 2048 / (warps(threads) * regs) : 1;
+  }
+  static constexpr int row_minb = PL::kStatic ? minb(row_threads, 128) : 1;
+  static constexpr int col_minb = PL::kStatic ? minb(col_threads, sizeof(T) == 8 ? 255 : 168) : 1;
+  static constexpr int spec_minb = PL::kStatic ? minb(col_threads, 128) : 1;
+};
+
+// Dynamic plans: teams per CTA chosen for the most resident threads per SM.
+template <class K>
+int dyn_teams(K kern, int nt, size_t team_bytes, int max_teams, int min_teams, bool prefer_big) {
+  cudaFuncAttributes fa;
+  int maxthr = 1024;
+  if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) maxthr = fa.maxThreadsPerBlock;
+  int best = 1;
+  long best_thr = -1;
+  for (int P = 1; P <= 32; ++P) {
+    if (P > max_teams && P > min_teams) break;
+    if (P * nt > maxthr) break;
+    const size_t smem = (size_t)P * team_bytes;
+    if (smem > 227 * 1024) break;
+    if (set_smem(kern, smem) != cudaSuccess) break;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, P * nt, smem) != cudaSuccess) break;
+    long thr = (long)nb * P * nt;
+    if (P < min_teams) thr /= 2;
+    if (thr > best_thr || (thr == best_thr && prefer_big)) {
+      best = P;
+      best_thr = thr;
+    }
+  }
+  return best;
+}
+
+template <class PL, class K>
+int row_teams(K kern, const FFTDesc<typename PL::Scalar>& d, int nrows) {
+  using T = typename PL::Scalar;
+  if constexpr (PL::kStatic) return Shape<PL>::row_pairs;
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(d.L, (nrows + 1) / 2);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int P = dyn_teams(kern, PL::nt(d), (size_t)PL::slots(d.L) * sizeof(cplx<T>), (nrows + 1) / 2,
+                          sizeof(T) == 8 ? 1 : 2, true);
+  cache[key] = P;
   return P;
 }
 
-template <class T>
-int cols_per_cta(int nt, int L, int Hx) {
-  int C = Prec<T>::cols_threads / nt;
-  if (C < 1) C = 1;
-  while (C > 1 && (size_t)C * team_stride(L) * sizeof(cplx<T>) > 100 * 1024) --C;
-  if (C > Hx) C = Hx;
+template <class PL, class K>
+int col_teams(K kern, const FFTDesc<typename PL::Scalar>& d, int ncols) {
+  using T = typename PL::Scalar;
+  if constexpr (PL::kStatic) return Shape<PL>::col_teams;
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(d.L, ncols);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int C = dyn_teams(kern, PL::nt(d), (size_t)PL::slots(d.L) * sizeof(cplx<T>), ncols, 1, false);
+  cache[key] = C;
   return C;
-}
-
-}  // namespace
-
-#define BTTB_E_DISPATCH(E, ...)                        \
-  switch (E) {                                         \
-    case 8: { constexpr int EE = 8; __VA_ARGS__; } break;   \
-    case 12: { constexpr int EE = 12; __VA_ARGS__; } break; \
-    case 20: { constexpr int EE = 20; __VA_ARGS__; } break; \
-    default: return cudaErrorInvalidValue;             \
-  }
-
-template <class K>
-int team_limit(K kern, int nt) {
-  cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
-  return fa.maxThreadsPerBlock / nt > 0 ? fa.maxThreadsPerBlock / nt : 1;
 }
 
 template <class T>
 cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
-  BTTB_E_DISPATCH(E, {
-    auto kern = k_row_r2c<T, EE>;
-    int P = pairs_per_cta<T>(d.nt, d.L, a.nrows);
-    P = P < team_limit(kern, d.nt) ? P : team_limit(kern, d.nt);
-    const size_t smem = (size_t)P * team_stride(d.L) * sizeof(cplx<T>);
-    dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * d.nt);
+  return with_plan<T>(d.L, E, [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    auto kern = k_row_r2c<PL, Shape<PL>::row_threads, Shape<PL>::row_minb>;
+    const int P = row_teams<PL>(kern, d, a.nrows);
+    const size_t smem = (size_t)P * PL::slots(d.L) * sizeof(cplx<T>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
+    dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * PL::nt(d));
     kern<<<grd, blk, smem, st>>>(a, d, P);
+    return cudaGetLastError();
   });
-  return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
-  BTTB_E_DISPATCH(E, {
-    auto kern = k_row_c2r<T, EE>;
-    int P = pairs_per_cta<T>(d.nt, d.L, a.nrows);
-    P = P < team_limit(kern, d.nt) ? P : team_limit(kern, d.nt);
-    const size_t smem = (size_t)P * team_stride(d.L) * sizeof(cplx<T>);
-    dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * d.nt);
+  return with_plan<T>(d.L, E, [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    auto kern = k_row_c2r<PL, Shape<PL>::row_threads, Shape<PL>::row_minb>;
+    const int P = row_teams<PL>(kern, d, a.nrows);
+    const size_t smem = (size_t)P * PL::slots(d.L) * sizeof(cplx<T>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
+    dim3 grd((a.nrows + 2 * P - 1) / (2 * P), a.nslabs), blk(P * PL::nt(d));
     kern<<<grd, blk, smem, st>>>(a, d, P);
+    return cudaGetLastError();
   });
-  return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
-  BTTB_E_DISPATCH(E, {
-    auto kern = k_col_fwd<T, EE>;
-    int C = cols_per_cta<T>(d.nt, d.L, a.Hx);
-    C = C < team_limit(kern, d.nt) ? C : team_limit(kern, d.nt);
-    const size_t smem = (size_t)C * team_stride(d.L) * sizeof(cplx<T>);
-    dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * d.nt);
+  return with_plan<T>(d.L, E, [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    auto kern = k_col_fwd<PL, Shape<PL>::col_threads, Shape<PL>::col_minb>;
+    const int C = col_teams<PL>(kern, d, a.Hx);
+    const size_t smem = (size_t)C * PL::slots(d.L) * sizeof(cplx<T>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
+    dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * PL::nt(d));
     kern<<<grd, blk, smem, st>>>(a, d, C);
+    return cudaGetLastError();
   });
-  return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
-  BTTB_E_DISPATCH(E, {
-    auto kern = k_col_tra<T, EE>;
-    int C = cols_per_cta<T>(d.nt, d.L, a.Hx);
-    C = C < team_limit(kern, d.nt) ? C : team_limit(kern, d.nt);
-    const size_t smem = (size_t)C * team_stride(d.L) * sizeof(cplx<T>);
-    dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * d.nt);
+  return with_plan<T>(d.L, E, [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    auto kern = k_col_tra<PL, Shape<PL>::col_threads, Shape<PL>::col_minb>;
+    const int C = col_teams<PL>(kern, d, a.Hx);
+    const size_t smem = (size_t)C * PL::slots(d.L) * sizeof(cplx<T>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
+    dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * PL::nt(d));
     kern<<<grd, blk, smem, st>>>(a, d, C);
+    return cudaGetLastError();
   });
-  return cudaGetLastError();
 }
 
 template <class TS>
 cudaError_t launch_col_spec(const ColSpecArgs& a, const FFTDesc<double>& d, int E, cudaStream_t st) {
-  BTTB_E_DISPATCH(E, {
-    auto kern = k_col_spec<TS, EE>;
-    int C = cols_per_cta<double>(d.nt, d.L, a.Hx);
-    C = C < team_limit(kern, d.nt) ? C : team_limit(kern, d.nt);
-    const size_t smem = (size_t)C * team_stride(d.L) * sizeof(double2);
-    dim3 grd((a.Hx + C - 1) / C), blk(C * d.nt);
+  return with_plan<double>(d.L, E, [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    auto kern = k_col_spec<PL, TS, Shape<PL>::col_threads, Shape<PL>::spec_minb>;
+    const int C = col_teams<PL>(kern, d, a.Hx);
+    const size_t smem = (size_t)C * PL::slots(d.L) * sizeof(double2);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
+    dim3 grd((a.Hx + C - 1) / C), blk(C * PL::nt(d));
     kern<<<grd, blk, smem, st>>>(a, d, C);
+    return cudaGetLastError();
   });
-  return cudaGetLastError();
 }
 
 template cudaError_t launch_row_r2c<double>(const RowR2CArgs&, const FFTDesc<double>&, int, cudaStream_t);
