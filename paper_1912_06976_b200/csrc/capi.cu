@@ -182,6 +182,8 @@ size_t chunk_budget() {
   return (size_t)64 << 20;
 }
 
+size_t round_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
+
 }  // namespace
 
 struct bttb_plan_s {
@@ -195,7 +197,11 @@ struct bttb_plan_s {
   FFTPlanHost fx, fy;
   size_t elem = 16;
   void* spectra = nullptr;
-  DevBuf ybuf, wbuf, hin, hout;
+  DevBuf work, hin, hout;
+  cudaStream_t stream = nullptr;  // internal stream carrying the L2 persisting window
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  void* window_base = nullptr;
+  size_t window_bytes = 0;
   int64_t last_K = 0, last_G = 0, last_launches = 0;
   std::mutex mu;
 
@@ -354,6 +360,32 @@ int build_spectra(bttb_plan_s* p) {
   return rc;
 }
 
+// Persisting L2 window over the chunk workspace (device-wide persisting
+// carve-out raised to cover it, capped by the hardware maximum).
+int set_l2_window(bttb_plan_s* p, void* base, size_t bytes) {
+  if (getenv("BTTB_NO_L2_WINDOW")) return BTTB_OK;
+  if (base == p->window_base && bytes == p->window_bytes) return BTTB_OK;
+  int maxwin = 0, maxpersist = 0;
+  CU(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
+  CU(cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, p->device));
+  if (maxwin <= 0 || maxpersist <= 0) return BTTB_OK;
+  size_t cur = 0;
+  CU(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  const size_t want = std::min(bytes, (size_t)maxpersist);
+  if (cur < want) CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  CU(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = base;
+  v.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)maxwin);
+  v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)cur / (double)v.accessPolicyWindow.num_bytes);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  CU(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  p->window_base = base;
+  p->window_bytes = bytes;
+  return BTTB_OK;
+}
+
 template <class T>
 int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st) {
   using V = cplx<T>;
@@ -366,13 +398,17 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
   int64_t G = 1;
   if (K == p->nzl) G = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(budget / (slab * p->nzl))));
   int rc;
-  if ((rc = p->ybuf.ensure(slab * K * G))) return rc;
-  if ((rc = p->wbuf.ensure((size_t)Hx * sy * sizeof(V) * G))) return rc;
+  // one workspace: the chunk intermediate Y (row-pass output / transposed
+  // column output) then the accumulator / data half-spectrum W; both are kept
+  // L2-resident by the persisting access-policy window on the plan's stream
+  const size_t ybytes = round_up(slab * K * G, 4096), wbytes = round_up((size_t)Hx * sy * sizeof(V) * G, 4096);
+  if ((rc = p->work.ensure(ybytes + wbytes))) return rc;
+  if ((rc = set_l2_window(p, p->work.p, ybytes + wbytes))) return rc;
   p->last_K = K;
   p->last_G = G;
   int64_t launches = 0;
-  V* Yb = static_cast<V*>(p->ybuf.p);
-  V* Wb = static_cast<V*>(p->wbuf.p);
+  V* Yb = static_cast<V*>(p->work.p);
+  V* Wb = reinterpret_cast<V*>(static_cast<char*>(p->work.p) + ybytes);
   const V* S = static_cast<const V*>(p->spectra);
   const long long s_rstride = (long long)Hx * p->Ly;
   for (int64_t b0 = 0; b0 < batch; b0 += G) {
@@ -494,8 +530,10 @@ void destroy_plan(bttb_plan_s* p) {
   if (p->spectra) cudaFree(p->spectra);
   p->fx.release();
   p->fy.release();
-  p->ybuf.release();
-  p->wbuf.release();
+  p->work.release();
+  if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
   p->hin.release();
   p->hout.release();
   delete p;
@@ -576,6 +614,12 @@ int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* 
       rc = fail(BTTB_ENOMEM, "cannot allocate %zu bytes of spectrum cache: %s", bytes, cudaGetErrorString(e));
     }
   }
+  if (!rc) {
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(BTTB_ECUDA, "cannot create the plan stream");
+  }
   if (!rc) rc = build_spectra(p);
   if (rc) {
     std::string msg = g_err;
@@ -616,9 +660,16 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   } else if (where != BTTB_DEVICE_PTR) {
     return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR or BTTB_HOST_PTR");
   }
-  int rc = p->dtype == BTTB_F64 ? run_apply<double>(p, mode, xd, yd, batch, st)
-                                : run_apply<float>(p, mode, xd, yd, batch, st);
+  // the work runs on the plan's stream (which carries the L2 window), ordered
+  // after everything already queued on the caller's stream and before
+  // anything the caller queues next
+  CU(cudaEventRecord(p->ev_in, st));
+  CU(cudaStreamWaitEvent(p->stream, p->ev_in, 0));
+  int rc = p->dtype == BTTB_F64 ? run_apply<double>(p, mode, xd, yd, batch, p->stream)
+                                : run_apply<float>(p, mode, xd, yd, batch, p->stream);
   if (rc) return rc;
+  CU(cudaEventRecord(p->ev_out, p->stream));
+  CU(cudaStreamWaitEvent(st, p->ev_out, 0));
   if (where == BTTB_HOST_PTR) {
     CU(cudaMemcpyAsync(y, yd, out_elems * esz, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));

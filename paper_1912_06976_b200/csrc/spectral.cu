@@ -17,11 +17,13 @@
 // they stay L2-resident between the row and column kernels.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
 
 #include "spectral.h"
+#include "tma.cuh"
 
 namespace bttb {
 
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_row_c2r(RowC2RArgs a, FFTDesc<ty
 // Forward column stage: FFT along y, multiply by cached spectrum, accumulate
 // over the chunk's layers in registers, one inverse FFT, extract stations.
 // ---------------------------------------------------------------------------
-template <class PL, int MAXT, int MINB>
+template <class PL, int MAXT, int MINB, bool ACCS>
 __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd(ColFwdArgs a, FFTDesc<typename PL::Scalar> d, int C) {
   using T = typename PL::Scalar;
   using V = cplx<T>;
@@ -151,10 +153,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd(ColFwdArgs a, FFTDesc<ty
   const bool kv = kx < a.Hx;
   const int kxc = kv ? kx : 0;
   const int b = blockIdx.y;
-  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * Ls;
-  V acc[E], v[E];
+  // team buffer: [exchange (Ls padded slots)] [+ accumulator, L slots, if ACCS]
+  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * (Ls + (ACCS ? d.L : 0));
+  V* accs = sm + Ls;  // thread t owns slots t + nt*k: conflict-free, no barrier needed
+  V acc[ACCS ? 1 : E], v[E];
+  if constexpr (!ACCS) {
 #pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
+    for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
+  }
   const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kxc * a.ldy;
   const V* Sb = static_cast<const V*>(a.S) + (long long)kxc * a.lds;
   for (int r = 0; r < a.K; ++r) {
@@ -169,20 +175,32 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd(ColFwdArgs a, FFTDesc<ty
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       const V w = __ldcs(sc + t + nt * k);
-      acc[k].x += w.x * v[k].x - w.y * v[k].y;
-      acc[k].y += w.x * v[k].y + w.y * v[k].x;
+      if constexpr (ACCS) {
+        V o = r == 0 ? mkc<V>(T(0), T(0)) : accs[t + nt * k];
+        o.x += w.x * v[k].x - w.y * v[k].y;
+        o.y += w.x * v[k].y + w.y * v[k].x;
+        accs[t + nt * k] = o;
+      } else {
+        acc[k].x += w.x * v[k].x - w.y * v[k].y;
+        acc[k].y += w.x * v[k].y + w.y * v[k].x;
+      }
     }
   }
+  if constexpr (ACCS) {
 #pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
-  PL::fft(acc, sm, t, d);
+    for (int k = 0; k < E; ++k) v[k] = conjv(accs[t + nt * k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = conjv(acc[k]);
+  }
+  PL::fft(v, sm, t, d);
   if (kv) {
     V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       const int j = t + nt * k;
       if (j < a.nout) {
-        V val = conjv(acc[k]);
+        V val = conjv(v[k]);
         if (a.accumulate) val = val + wc[j];
         wc[j] = val;
       }
@@ -194,7 +212,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd(ColFwdArgs a, FFTDesc<ty
 // Transpose column stage: FFT of the data column once, then per layer
 // conj(spectrum) multiply and inverse FFT, extract prism rows.
 // ---------------------------------------------------------------------------
-template <class PL, int MAXT, int MINB>
+template <class PL, int MAXT, int MINB, bool ACCS>
 __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<typename PL::Scalar> d, int C) {
   using T = typename PL::Scalar;
   using V = cplx<T>;
@@ -206,15 +224,20 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
   const bool kv = kx < a.Hx;
   const int kxc = kv ? kx : 0;
   const int b = blockIdx.y;
-  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * Ls;
-  V dh[E], v[E];
+  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * (Ls + (ACCS ? d.L : 0));
+  V* dhs = sm + Ls;  // data spectrum, thread-owned slots (ACCS)
+  V dh[ACCS ? 1 : E], v[E];
   const V* dc = static_cast<const V*>(a.D) + (long long)b * a.d_bstride + (long long)kxc * a.ldd;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int j = t + nt * k;
-    dh[k] = j < a.nvalid ? dc[j] : mkc<V>(T(0), T(0));
+    v[k] = j < a.nvalid ? dc[j] : mkc<V>(T(0), T(0));
   }
-  PL::fft(dh, sm, t, d);
+  PL::fft(v, sm, t, d);
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if constexpr (ACCS) dhs[t + nt * k] = v[k]; else dh[k] = v[k];
+  }
   const V* Sb = static_cast<const V*>(a.S) + (long long)kxc * a.lds;
   V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kxc * a.ldw;
   for (int r = 0; r < a.K; ++r) {
@@ -223,7 +246,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
     for (int k = 0; k < E; ++k) {
       // conj(conj(S) * dh) = S * conj(dh): inverse FFT via the conjugation identity
       const V w = __ldcs(sc + t + nt * k);
-      v[k] = mkc<V>(w.x * dh[k].x + w.y * dh[k].y, w.y * dh[k].x - w.x * dh[k].y);
+      V h;
+      if constexpr (ACCS) h = dhs[t + nt * k]; else h = dh[k];
+      v[k] = mkc<V>(w.x * h.x + w.y * h.y, w.y * h.x - w.x * h.y);
     }
     PL::fft(v, sm, t, d);
     if (kv) {
@@ -233,6 +258,143 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
         const int q = t + nt * k;
         if (q < a.nout) wc[q] = conjv(v[k]);
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined column stages (compile-time plans, one column per CTA).
+// Thread 0 streams the next layer's Y column and spectrum column into shared
+// memory with cp.async.bulk while the team runs the current FFT, so the
+// global-memory latency is off the critical path and the in-flight data
+// costs no registers.  Spectra are fetched with an L2 evict-first policy.
+// Shared layout: [exchange Ls][spectrum L][Y or D column nv][2 mbarriers].
+// ---------------------------------------------------------------------------
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDesc<typename PL::Scalar> d) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = PL::slots(L);
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* sbuf = sm + Ls;
+  V* ybuf = sbuf + L;
+  const int nv = a.nvalid;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ybuf + ((nv + 1) & ~1));
+  const int t = threadIdx.x;
+  const int kx = blockIdx.x, b = blockIdx.y;
+  const uint32_t ybytes = nv * sizeof(V), sbytes = L * sizeof(V);
+  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const uint64_t pol = policy_evict_first();
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bars[0], ybytes);
+    tma_load(ybuf, Yb, ybytes, &bars[0], pol);
+    mbar_arrive_expect_tx(&bars[1], sbytes);
+    tma_load(sbuf, Sb, sbytes, &bars[1], pol);
+  }
+  __syncthreads();
+  V acc[E], v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
+  for (int r = 0; r < a.K; ++r) {
+    mbar_wait(&bars[0], r & 1);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int q = t + NT * k;
+      v[k] = q < nv ? ybuf[q] : mkc<V>(T(0), T(0));
+    }
+    __syncthreads();
+    if (t == 0 && r + 1 < a.K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[0], ybytes);
+      tma_load(ybuf, Yb + (long long)(r + 1) * a.y_rstride, ybytes, &bars[0], pol);
+    }
+    PL::fft(v, sm, t, d);
+    mbar_wait(&bars[1], r & 1);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const V w = sbuf[t + NT * k];
+      acc[k].x += w.x * v[k].x - w.y * v[k].y;
+      acc[k].y += w.x * v[k].y + w.y * v[k].x;
+    }
+    __syncthreads();
+    if (t == 0 && r + 1 < a.K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[1], sbytes);
+      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[1], pol);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
+  PL::fft(acc, sm, t, d);
+  V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int j = t + NT * k;
+    if (j < a.nout) {
+      V val = conjv(acc[k]);
+      if (a.accumulate) val = val + wc[j];
+      wc[j] = val;
+    }
+  }
+}
+
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDesc<typename PL::Scalar> d) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = PL::slots(L);
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* sbuf = sm + Ls;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + L);
+  const int t = threadIdx.x;
+  const int kx = blockIdx.x, b = blockIdx.y;
+  const uint32_t sbytes = L * sizeof(V);
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const uint64_t pol = policy_evict_first();
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bars[0], sbytes);
+    tma_load(sbuf, Sb, sbytes, &bars[0], pol);
+  }
+  V dh[E], v[E];
+  const V* dc = static_cast<const V*>(a.D) + (long long)b * a.d_bstride + (long long)kx * a.ldd;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int j = t + NT * k;
+    dh[k] = j < a.nvalid ? dc[j] : mkc<V>(T(0), T(0));
+  }
+  __syncthreads();
+  PL::fft(dh, sm, t, d);
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
+  for (int r = 0; r < a.K; ++r) {
+    mbar_wait(&bars[0], r & 1);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      // conj(conj(S) * dh) = S * conj(dh): inverse FFT via the conjugation identity
+      const V w = sbuf[t + NT * k];
+      v[k] = mkc<V>(w.x * dh[k].x + w.y * dh[k].y, w.y * dh[k].x - w.x * dh[k].y);
+    }
+    __syncthreads();
+    if (t == 0 && r + 1 < a.K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[0], sbytes);
+      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[0], pol);
+    }
+    PL::fft(v, sm, t, d);
+    V* wc = Wb + (long long)r * a.w_rstride;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int q = t + NT * k;
+      if (q < a.nout) wc[q] = conjv(v[k]);
     }
   }
 }
@@ -324,9 +486,18 @@ template <class PL> struct Shape {
     return 2048 / (warps(threads) * regs) > 1 ? 2048 / (warps(threads) * regs) : 1;
   }
   static constexpr int row_minb = PL::kStatic ? minb(row_threads, 128) : 1;
-  static constexpr int col_minb = PL::kStatic ? minb(col_threads, sizeof(T) == 8 ? 255 : 168) : 1;
+  // fp64 plans with 20 elements per thread keep the column accumulator in
+  // shared memory (registers would cap occupancy at two teams per SM)
+  static constexpr bool acc_smem = false;  // measured slower on C4 fp64 (10.6 vs 9.8 ms/step)
+  static constexpr int col_minb = PL::kStatic ? minb(col_threads, acc_smem ? 168 : (sizeof(T) == 8 ? 255 : 168)) : 1;
   static constexpr int spec_minb = PL::kStatic ? minb(col_threads, 128) : 1;
+  static constexpr int tma_minb = PL::kStatic ? minb(col_threads, sizeof(T) == 8 ? 255 : 168) : 1;
 };
+
+bool tma_ok() {
+  static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
+  return ok;
+}
 
 // Dynamic plans: teams per CTA chosen for the most resident threads per SM.
 template <class K>
@@ -422,9 +593,23 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    auto kern = k_col_fwd<PL, Shape<PL>::col_threads, Shape<PL>::col_minb>;
+    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+      const size_t esz = sizeof(cplx<T>);
+      if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
+          (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
+        auto kern = k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
+        const size_t smem = (size_t)(PL::slots(d.L) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
+        kern<<<grd, blk, smem, st>>>(a, d);
+        return cudaGetLastError();
+      }
+    }
+    constexpr bool accs = Shape<PL>::acc_smem;
+    auto kern = k_col_fwd<PL, Shape<PL>::col_threads, Shape<PL>::col_minb, accs>;
     const int C = col_teams<PL>(kern, d, a.Hx);
-    const size_t smem = (size_t)C * PL::slots(d.L) * sizeof(cplx<T>);
+    const size_t smem = (size_t)C * (PL::slots(d.L) + (accs ? d.L : 0)) * sizeof(cplx<T>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * PL::nt(d));
@@ -438,9 +623,22 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    auto kern = k_col_tra<PL, Shape<PL>::col_threads, Shape<PL>::col_minb>;
+    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+      const size_t esz = sizeof(cplx<T>);
+      if (tma_ok() && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
+        auto kern = k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
+        const size_t smem = (size_t)(PL::slots(d.L) + d.L) * esz + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
+        kern<<<grd, blk, smem, st>>>(a, d);
+        return cudaGetLastError();
+      }
+    }
+    constexpr bool accs = Shape<PL>::acc_smem;
+    auto kern = k_col_tra<PL, Shape<PL>::col_threads, Shape<PL>::col_minb, accs>;
     const int C = col_teams<PL>(kern, d, a.Hx);
-    const size_t smem = (size_t)C * PL::slots(d.L) * sizeof(cplx<T>);
+    const size_t smem = (size_t)C * (PL::slots(d.L) + (accs ? d.L : 0)) * sizeof(cplx<T>);
     cudaError_t e = set_smem(kern, smem);
     if (e != cudaSuccess) return e;
     dim3 grd((a.Hx + C - 1) / C, a.nbatch), blk(C * PL::nt(d));

@@ -28,3 +28,8 @@ for name in ["C1", "C2", "C3"]:
     p = GRAV if kind == "gravity" else B.KernelParams.magnetic(*O.CONFIGS[name][11])
     run(name, g, kind, c, p)
     run(name, g, kind, c, p, "float32")
+# C4 geometry, 3 layers (TMA column path at L=2000), fp64 and fp32
+g = O.config_grid("C4", nz=3); kind, c = O.config_kernel("C4")
+p = B.KernelParams.magnetic(*O.CONFIGS["C4"][11])
+run("C4[3 layers]", g, kind, c, p)
+run("C4[3 layers]", g, kind, c, p, "float32")
