@@ -371,3 +371,52 @@ def forward_threaded(g, fw, x, pool):
 def transpose_threaded(g, tr, v, pool):
     parts = list(pool.map(lambda T: transpose(g, [T], v), tr))
     return np.concatenate(parts)
+
+
+# --------------------------------------------------------------------------
+# independent per-entry dense operator (restates pkg/tests/oracles.py:13-69):
+# scalar corner sums with distances recomputed for every station/prism pair,
+# no tables, no Toeplitz structure -- a second, structurally different oracle.
+# --------------------------------------------------------------------------
+def _prism_gravity(x1, x2, y1, y2, z1, z2, gs):
+    from math import atan2, log, sqrt
+    tot = 0.0
+    for i, x in enumerate((x1, x2)):
+        for j, y in enumerate((y1, y2)):
+            for k, z in enumerate((z1, z2)):
+                rho = sqrt(x * x + y * y + z * z)
+                tot += (-1.0) ** (i + j + k + 1) * (z * atan2(x * y, z * rho)
+                                                    - x * log(rho + y) - y * log(rho + x))
+    return gs * tot
+
+
+def _prism_magnetic(x1, x2, y1, y2, z1, z2, gc):
+    from math import atan2, log, sqrt
+    tot = 0.0
+    for i, x in enumerate((x1, x2)):
+        for j, y in enumerate((y1, y2)):
+            for k, z in enumerate((z1, z2)):
+                rho = sqrt(x * x + y * y + z * z)
+                tot += (-1.0) ** (i + j + k + 1) * (
+                    gc[0] * log(rho + x) + gc[1] * log(rho + y) + gc[2] * log(rho + z)
+                    + gc[3] * atan2(x * z, rho * y) + gc[4] * atan2(y * z, rho * x))
+    return tot
+
+
+def dense_layers(g, kind, consts):
+    """Per-layer m x n_r matrices, one scalar kernel call per entry (small grids only)."""
+    out = []
+    for r in range(g.nz):
+        z1, z2 = g.z[r], g.z[r + 1]
+        G = np.zeros((g.m, g.n_r))
+        for j in range(g.sy):
+            b = (g.pyl + j + 0.5) * g.dy
+            for i in range(g.sx):
+                a = (g.pxl + i + 0.5) * g.dx
+                for q in range(g.ny):
+                    for p in range(g.nx):
+                        args = (p * g.dx - a, (p + 1) * g.dx - a, q * g.dy - b, (q + 1) * g.dy - b, z1, z2)
+                        G[j * g.sx + i, q * g.nx + p] = (_prism_gravity(*args, consts) if kind == "gravity"
+                                                         else _prism_magnetic(*args, consts))
+        out.append(G)
+    return out
