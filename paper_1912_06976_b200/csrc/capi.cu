@@ -58,10 +58,20 @@ int length_family(int64_t L) {  // returns E (elements per thread) or 0
   return 0;
 }
 
+// Smallest supported length >= n.  BTTB_FFT_POW2=1 prefers a power of two
+// within 5% of it: tools/fftbench.cu measures 2048 at 1.16x (fp64) / 1.8x
+// (fp32) the per-point FFT rate of 2000, but the fused C4 operator measured
+// slower at 2048 (fp64 11.4 vs 8.5 ms/step), so it is off by default.
 int64_t pick_length(int64_t n) {
+  int64_t best = -1;
   for (int64_t L = std::max<int64_t>(n, 8); L <= 8192; ++L)
-    if (length_family(L)) return L;
-  return -1;
+    if (length_family(L)) { best = L; break; }
+  if (best < 0) return -1;
+  static const bool pow2 = getenv("BTTB_FFT_POW2") && atoi(getenv("BTTB_FFT_POW2")) != 0;
+  int64_t p2 = 8;
+  while (p2 < n) p2 *= 2;
+  if (pow2 && p2 <= 8192 && p2 * 100 <= best * 105) return p2;
+  return best;
 }
 
 // Radix plan of one length at one precision: E elements per thread
@@ -183,6 +193,12 @@ size_t chunk_budget() {
 }
 
 size_t round_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
+
+// transpose intermediate layout: row-major [q][kx] (BTTB_TRA_ROWMAJOR=1) or [kx][q]
+bool tra_rowmajor() {
+  static const bool rm = getenv("BTTB_TRA_ROWMAJOR") && atoi(getenv("BTTB_TRA_ROWMAJOR")) != 0;
+  return rm;
+}
 
 }  // namespace
 
@@ -392,7 +408,8 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
   const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
   const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
                 nloc = p->nloc();
-  const size_t slab = (size_t)Hx * ny * sizeof(V);
+  const int64_t Hxp = (Hx + 1) & ~int64_t(1);  // row length of the row-major transpose intermediate
+  const size_t slab = (size_t)Hxp * ny * sizeof(V);
   const size_t budget = chunk_budget();
   int64_t K = std::max<int64_t>(1, std::min<int64_t>(p->nzl, (int64_t)(budget / slab)));
   int64_t G = 1;
@@ -495,17 +512,18 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.lds = (int)p->Ly;
         ca.K = k;
         ca.W = Yb;
-        ca.w_bstride = (long long)k * Hx * ny;
-        ca.w_rstride = (long long)Hx * ny;
-        ca.ldw = (int)ny;
+        ca.w_bstride = (long long)k * Hxp * ny;
+        ca.w_rstride = (long long)Hxp * ny;
+        ca.rowmajor = tra_rowmajor() ? 1 : 0;
+        ca.ldw = ca.rowmajor ? (int)Hxp : (int)ny;  // row-major [q][kx]: the C2R pass reads contiguous rows
         ca.nout = (int)ny;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
         CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), st));
         RowC2RArgs oa{};
         oa.in = Yb;
-        oa.in_sstride = (long long)Hx * ny;
-        oa.ld_in = (int)ny;
+        oa.in_sstride = (long long)Hxp * ny;
+        oa.ld_in = ca.rowmajor ? (int)Hxp : (int)ny;
         oa.nrows = (int)ny;
         oa.Hx = (int)Hx;
         oa.nslabs = gb * k;
@@ -515,6 +533,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         oa.spb = k;
         oa.ld_out = (int)nx;
         oa.nout = (int)nx;
+        oa.rowmajor = ca.rowmajor;
         CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
         launches += 2;
       }

@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_row_c2r(RowC2RArgs a, FFTDesc<ty
   for (int it = tid; it < nitems; it += blockDim.x) {
     const int kx = it / P, cc = it - kx * P;
     const int j = j0 + 2 * cc;
-    const V* p = in + (long long)kx * a.ld_in + j;
+    const V* p = a.rowmajor ? in + (long long)j * a.ld_in + kx : in + (long long)kx * a.ld_in + j;
     V A = j < a.nrows ? p[0] : mkc<V>(T(0), T(0));
-    V B = j + 1 < a.nrows ? p[1] : mkc<V>(T(0), T(0));
+    V B = j + 1 < a.nrows ? p[a.rowmajor ? a.ld_in : 1] : mkc<V>(T(0), T(0));
     if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
       A.y = T(0);
       B.y = T(0);
@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
     if constexpr (ACCS) dhs[t + nt * k] = v[k]; else dh[k] = v[k];
   }
   const V* Sb = static_cast<const V*>(a.S) + (long long)kxc * a.lds;
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kxc * a.ldw;
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kxc * (a.rowmajor ? 1 : a.ldw);
+  const long long qstride = a.rowmajor ? a.ldw : 1;
   for (int r = 0; r < a.K; ++r) {
     const V* sc = Sb + (long long)r * a.s_rstride;
 #pragma unroll
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         const int q = t + nt * k;
-        if (q < a.nout) wc[q] = conjv(v[k]);
+        if (q < a.nout) wc[q * qstride] = conjv(v[k]);
       }
     }
   }
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   using V = cplx<T>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = PL::slots(L);
+  const int Ls = (PL::slots(L) + 1) & ~1;  // keep the TMA staging buffers 16-byte aligned
   V* sm = reinterpret_cast<V*>(smraw);
   V* sbuf = sm + Ls;
   V* ybuf = sbuf + L;
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
   using V = cplx<T>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = PL::slots(L);
+  const int Ls = (PL::slots(L) + 1) & ~1;  // keep the TMA staging buffers 16-byte aligned
   V* sm = reinterpret_cast<V*>(smraw);
   V* sbuf = sm + Ls;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + L);
@@ -374,7 +375,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
   }
   __syncthreads();
   PL::fft(dh, sm, t, d);
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw);
+  const long long qstride = a.rowmajor ? a.ldw : 1;
   for (int r = 0; r < a.K; ++r) {
     mbar_wait(&bars[0], r & 1);
 #pragma unroll
@@ -394,7 +396,270 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       const int q = t + NT * k;
-      if (q < a.nout) wc[q] = conjv(v[k]);
+      if (q < a.nout) wc[q * qstride] = conjv(v[k]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent, TMA double-buffered row passes (compile-time plans, one row pair
+// per iteration, one team per CTA).  Thread 0 bulk-copies the rows of the pair
+// two iterations ahead into the stage just consumed, so the contiguous row
+// loads overlap the FFTs.  Shared layout:
+//   [exchange Ls V][stage 0: row a, row b][stage 1: row a, row b][2 mbarriers]
+// ---------------------------------------------------------------------------
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_row_r2c_tma(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, int rowcap) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = (PL::slots(L) + 1) & ~1;  // keep the TMA staging buffers 16-byte aligned
+  V* sm = reinterpret_cast<V*>(smraw);
+  T* stage0 = reinterpret_cast<T*>(sm + Ls);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + 4 * rowcap);
+  const int t = threadIdx.x;
+  const int npairs = (a.nrows + 1) / 2, total = npairs * a.nslabs;
+  const uint64_t pol = policy_evict_first();
+  auto row_ptr = [&](int item, int which) {
+    const int s = item / npairs, q = 2 * (item - s * npairs) + which;
+    return static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride + (long long)(s % a.spb) * a.in_sstride +
+           (long long)q * a.ld_in;
+  };
+  auto has_b = [&](int item) { return 2 * (item % npairs) + 1 < a.nrows; };
+  auto issue = [&](int item, int st) {
+    const uint32_t bytes = a.nvalid * sizeof(T);
+    T* dst = stage0 + st * 2 * rowcap;
+    const bool b2 = has_b(item);
+    mbar_arrive_expect_tx(&bars[st], b2 ? 2 * bytes : bytes);
+    tma_load(dst, row_ptr(item, 0), bytes, &bars[st], pol);
+    if (b2) tma_load(dst + rowcap, row_ptr(item, 1), bytes, &bars[st], pol);
+  };
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < total) issue(blockIdx.x + gridDim.x, 1);
+  }
+  __syncthreads();
+  V v[E];
+  int it = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+    const int st = it & 1;
+    mbar_wait(&bars[st], (it >> 1) & 1);
+    const T* ra = stage0 + st * 2 * rowcap;
+    const T* rb = ra + rowcap;
+    const bool vb = has_b(item);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int i = t + NT * k;
+      const bool inb = i < a.nvalid;
+      v[k] = mkc<V>(inb ? ra[i] : T(0), inb && vb ? rb[i] : T(0));
+    }
+    __syncthreads();
+    if (t == 0 && item + 2 * (int)gridDim.x < total) {
+      fence_proxy_async();
+      issue(item + 2 * gridDim.x, st);
+    }
+    PL::fft(v, sm, t, d);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
+    __syncthreads();
+    const int s = item / npairs, q = 2 * (item - s * npairs);
+    V* out = static_cast<V*>(a.out) + (long long)s * a.out_sstride + q;
+    for (int kx = t; kx < a.Hx; kx += NT) {
+      const V zk = sm[PL::slot(kx)];
+      const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
+      const T h = T(0.5);
+      V* o = out + (long long)kx * a.ld_out;
+      o[0] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
+      if (vb) o[1] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+    }
+  }
+}
+
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_row_c2r_tma(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, int rowcap) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = (PL::slots(L) + 1) & ~1;  // keep the TMA staging buffers 16-byte aligned
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* stage0 = sm + Ls;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + 4 * rowcap);
+  const int t = threadIdx.x;
+  const int npairs = (a.nrows + 1) / 2, total = npairs * a.nslabs;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t bytes = rowcap * sizeof(V);
+  auto row_ptr = [&](int item, int which) {
+    const int s = item / npairs, j = 2 * (item - s * npairs) + which;
+    return static_cast<const V*>(a.in) + (long long)s * a.in_sstride + (long long)j * a.ld_in;
+  };
+  auto has_b = [&](int item) { return 2 * (item % npairs) + 1 < a.nrows; };
+  auto issue = [&](int item, int st) {
+    V* dst = stage0 + st * 2 * rowcap;
+    const bool b2 = has_b(item);
+    mbar_arrive_expect_tx(&bars[st], b2 ? 2 * bytes : bytes);
+    tma_load(dst, row_ptr(item, 0), bytes, &bars[st], pol);
+    if (b2) tma_load(dst + rowcap, row_ptr(item, 1), bytes, &bars[st], pol);
+  };
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < total) issue(blockIdx.x + gridDim.x, 1);
+  }
+  __syncthreads();
+  V v[E];
+  int it = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+    const int st = it & 1;
+    mbar_wait(&bars[st], (it >> 1) & 1);
+    const V* ra = stage0 + st * 2 * rowcap;
+    const V* rb = ra + rowcap;
+    const bool vb = has_b(item);
+    // build Z = A + iB over the full length from the two half spectra
+    for (int kx = t; kx < a.Hx; kx += NT) {
+      V A = ra[kx];
+      V B = vb ? rb[kx] : mkc<V>(T(0), T(0));
+      if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
+        A.y = T(0);
+        B.y = T(0);
+      }
+      sm[PL::slot(kx)] = mkc<V>(A.x - B.y, A.y + B.x);
+      if (kx >= 1 && kx <= L - a.Hx) sm[PL::slot(L - kx)] = mkc<V>(A.x + B.y, B.x - A.y);
+    }
+    __syncthreads();
+    if (t == 0 && item + 2 * (int)gridDim.x < total) {
+      fence_proxy_async();
+      issue(item + 2 * gridDim.x, st);
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = conjv(sm[PL::slot(t + NT * k)]);
+    PL::fft(v, sm, t, d);
+    const int s = item / npairs, j = 2 * (item - s * npairs);
+    T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
+    T* oa = out + (long long)j * a.ld_out;
+    T* ob = oa + a.ld_out;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int i = t + NT * k;
+      if (i < a.nout) {
+        __stcs(oa + i, v[k].x);
+        if (vb) __stcs(ob + i, -v[k].y);
+      }
+    }
+    __syncthreads();  // the next fill overwrites sm
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row passes with tensor-TMA transposed tiles (compile-time plans, one row
+// pair per CTA).  The pair's half spectra form a [kx][2 rows] box of the
+// transposed intermediate; it is staged in shared memory and moved by
+// cp.async.bulk.tensor (store for R2C, load for C2R) instead of one
+// 16-byte access per lane into a different L2 line.
+// Shared layout: [exchange Lsa][stage Hx x 2 complex][mbarrier].
+// ---------------------------------------------------------------------------
+constexpr int kBoxKx = 256;  // TMA box extent along kx (hardware maximum)
+
+template <class V> __host__ __device__ __forceinline__ int stage_offset(int slots) {
+  // 128-byte aligned start of the staging tile
+  const int per = 128 / (int)sizeof(V);
+  return (slots + per - 1) / per * per;
+}
+
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+    k_row_r2c_t2d(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap omap) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* stage = sm + stage_offset<V>(PL::slots(L));
+  const int t = threadIdx.x, s = blockIdx.y, qa = 2 * blockIdx.x, qb = qa + 1;
+  const T* in = static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride +
+                (long long)(s % a.spb) * a.in_sstride;
+  const bool vb = qb < a.nrows;
+  const T* ra = in + (long long)qa * a.ld_in;
+  const T* rb = in + (long long)(vb ? qb : qa) * a.ld_in;
+  V v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int i = t + NT * k;
+    const bool inb = i < a.nvalid;
+    v[k] = mkc<V>(inb ? __ldcs(ra + i) : T(0), vb && inb ? __ldcs(rb + i) : T(0));
+  }
+  PL::fft(v, sm, t, d);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
+  __syncthreads();
+  const T h = T(0.5);
+  for (int kx = t; kx < a.Hx; kx += NT) {
+    const V zk = sm[PL::slot(kx)];
+    const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
+    stage[2 * kx] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
+    stage[2 * kx + 1] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+  }
+  fence_proxy_async();
+  __syncthreads();
+  if (t == 0) {
+    for (int kx0 = 0; kx0 < a.Hx; kx0 += kBoxKx) tma_store_3d(&omap, stage + 2 * kx0, 2 * qa, kx0, s);
+    tma_store_commit();
+    tma_store_wait_read();
+  }
+}
+
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+    k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* stage = sm + stage_offset<V>(PL::slots(L));
+  const int nbox = (a.Hx + kBoxKx - 1) / kBoxKx;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + 2 * nbox * kBoxKx);
+  const int t = threadIdx.x, s = blockIdx.y, ja = 2 * blockIdx.x, jb = ja + 1;
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, (uint32_t)(nbox * kBoxKx * 2 * sizeof(V)));
+    for (int b = 0; b < nbox; ++b) tma_load_3d(stage + 2 * b * kBoxKx, &imap, 2 * ja, b * kBoxKx, s, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  for (int kx = t; kx < a.Hx; kx += NT) {
+    V A = stage[2 * kx], B = stage[2 * kx + 1];  // out-of-range rows arrive zero-filled
+    if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
+      A.y = T(0);
+      B.y = T(0);
+    }
+    sm[PL::slot(kx)] = mkc<V>(A.x - B.y, A.y + B.x);
+    if (kx >= 1 && kx <= L - a.Hx) sm[PL::slot(L - kx)] = mkc<V>(A.x + B.y, B.x - A.y);
+  }
+  __syncthreads();
+  V v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) v[k] = conjv(sm[PL::slot(t + NT * k)]);
+  PL::fft(v, sm, t, d);
+  const bool vb = jb < a.nrows;
+  T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
+  T* oa = out + (long long)ja * a.ld_out;
+  T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int i = t + NT * k;
+    if (i < a.nout) {
+      __stcs(oa + i, v[k].x);
+      if (vb) __stcs(ob + i, -v[k].y);
     }
   }
 }
@@ -436,6 +701,7 @@ template <class T, class F>
 cudaError_t with_plan(int L, int E, F&& f) {
   if constexpr (sizeof(T) == 8) {
     switch (L) {
+      case 2048: return f(Tag<SPlan<double, 8, 8, 8, 8, 8, 4>>{});
       case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
       case 512: return f(Tag<SPlan<double, 8, 8, 8, 8, 8>>{});
       case 432: return f(Tag<SPlan<double, 12, 12, 12, 12, 3>>{});
@@ -453,6 +719,7 @@ cudaError_t with_plan(int L, int E, F&& f) {
     }
   } else {
     switch (L) {
+      case 2048: return f(Tag<SPlan<float, 16, 16, 16, 16, 8>>{});
       case 2000: return f(Tag<SPlan<float, 20, 80, 20, 20, 5>>{});
       case 512: return f(Tag<SPlan<float, 8, 16, 8, 8, 8>>{});
       case 432: return f(Tag<SPlan<float, 12, 36, 12, 12, 3>>{});
@@ -485,17 +752,29 @@ template <class PL> struct Shape {
   static constexpr int minb(int threads, int regs) {
     return 2048 / (warps(threads) * regs) > 1 ? 2048 / (warps(threads) * regs) : 1;
   }
+  // register targets: the column kernels keep E-element accumulators beside the data
+  static constexpr int col_regs = 64 + 4 * PL::E * (int)(sizeof(T) / 4) > 255 ? 255 : 64 + 4 * PL::E * (int)(sizeof(T) / 4);
+  static constexpr int col_regs_rounded = col_regs <= 128 ? 128 : (col_regs <= 168 ? 168 : 255);
   static constexpr int row_minb = PL::kStatic ? minb(row_threads, 128) : 1;
   // fp64 plans with 20 elements per thread keep the column accumulator in
   // shared memory (registers would cap occupancy at two teams per SM)
   static constexpr bool acc_smem = false;  // measured slower on C4 fp64 (10.6 vs 9.8 ms/step)
-  static constexpr int col_minb = PL::kStatic ? minb(col_threads, acc_smem ? 168 : (sizeof(T) == 8 ? 255 : 168)) : 1;
+  static constexpr int col_minb = PL::kStatic ? minb(col_threads, acc_smem ? 168 : col_regs_rounded) : 1;
   static constexpr int spec_minb = PL::kStatic ? minb(col_threads, 128) : 1;
-  static constexpr int tma_minb = PL::kStatic ? minb(col_threads, sizeof(T) == 8 ? 255 : 168) : 1;
+  static constexpr int tma_minb = PL::kStatic ? minb(col_threads, col_regs_rounded) : 1;
+  static constexpr int rowtma_minb = PL::kStatic ? minb(NT, 128) : 1;
+  static constexpr int t2d_minb = PL::kStatic ? minb(NT, 128) : 1;
 };
 
 bool tma_ok() {
   static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
+  return ok;
+}
+
+// persistent TMA row passes: opt-in (BTTB_ROW_TMA=1); measured slower than the
+// one-CTA-per-pair kernels on C4 (8.73 vs 8.50 ms/step fp64)
+bool row_tma_ok() {
+  static const bool ok = tma_ok() && getenv("BTTB_ROW_TMA") && atoi(getenv("BTTB_ROW_TMA")) != 0;
   return ok;
 }
 
@@ -556,11 +835,97 @@ int col_teams(K kern, const FFTDesc<typename PL::Scalar>& d, int ncols) {
   return C;
 }
 
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+bool t2d_ok() {
+  static const bool ok = tma_ok() && encode_fn() != nullptr && !(getenv("BTTB_T2D") && atoi(getenv("BTTB_T2D")) == 0);
+  return ok;
+}
+
+// View of a transposed [slab][kx][row] complex array as reals: dims (2*rows, Hx,
+// slabs), box (4 reals = 2 rows, 256 kx, 1 slab).
+template <class T>
+bool encode_rowpair_map(CUtensorMap* m, const void* base, int rows, int Hx, int slabs, long long ld_kx,
+                        long long ld_slab) {
+  const size_t esz = sizeof(T);
+  if (!al16(base) || (ld_kx * 2 * esz) % 16 || (ld_slab * 2 * esz) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)2 * rows, (cuuint64_t)Hx, (cuuint64_t)slabs};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld_kx * 2 * esz), (cuuint64_t)(ld_slab * 2 * esz)};
+  cuuint32_t box[3] = {4, (cuuint32_t)(Hx < kBoxKx ? Hx : kBoxKx), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                 const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// grid of a persistent kernel: every SM filled to its occupancy, never more CTAs than items
+template <class K>
+int persistent_grid(K kern, int threads, size_t smem, int items) {
+  int nb = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess || nb < 1) nb = 1;
+  const int g = nb * sm_count();
+  return items < g ? items : g;
+}
+
 template <class T>
 cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
   return with_plan<T>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
+    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+      const size_t esz = sizeof(T);
+      if (row_tma_ok() && al16(a.in) && (a.nvalid * esz) % 16 == 0 && (a.ld_in * esz) % 16 == 0 &&
+          (a.in_sstride * esz) % 16 == 0 && (a.in_bstride * esz) % 16 == 0) {
+        auto kern = k_row_r2c_tma<PL, PL::NT, Shape<PL>::rowtma_minb>;
+        const int rowcap = (a.nvalid + 1) & ~1;
+        const size_t smem = (size_t)((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 4 * (size_t)rowcap * esz + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        const int items = (a.nrows + 1) / 2 * a.nslabs;
+        kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, rowcap);
+        return cudaGetLastError();
+      }
+      CUtensorMap omap;
+      if (t2d_ok() && a.Hx <= 65535 &&
+          encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride)) {
+        auto kern = k_row_r2c_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
+        const size_t smem = (size_t)(stage_offset<cplx<T>>(PL::slots(d.L)) + 2 * a.Hx) * sizeof(cplx<T>);
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd((a.nrows + 1) / 2, a.nslabs);
+        kern<<<grd, PL::NT, smem, st>>>(a, d, omap);
+        return cudaGetLastError();
+      }
+    }
     auto kern = k_row_r2c<PL, Shape<PL>::row_threads, Shape<PL>::row_minb>;
     const int P = row_teams<PL>(kern, d, a.nrows);
     const size_t smem = (size_t)P * PL::slots(d.L) * sizeof(cplx<T>);
@@ -577,6 +942,32 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
   return with_plan<T>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
+    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+      const size_t esz = sizeof(cplx<T>);
+      const int rowcap = (a.Hx + 1) & ~1;
+      if (row_tma_ok() && a.rowmajor && al16(a.in) && a.ld_in >= rowcap && (a.ld_in * esz) % 16 == 0 &&
+          (rowcap * esz) % 16 == 0 && (a.in_sstride * esz) % 16 == 0) {
+        auto kern = k_row_c2r_tma<PL, PL::NT, Shape<PL>::rowtma_minb>;
+        const size_t smem = (size_t)((PL::slots(d.L) + 1) & ~1) * esz + 4 * (size_t)rowcap * esz + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        const int items = (a.nrows + 1) / 2 * a.nslabs;
+        kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, rowcap);
+        return cudaGetLastError();
+      }
+      CUtensorMap imap;
+      if (t2d_ok() && !a.rowmajor &&
+          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride)) {
+        auto kern = k_row_c2r_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
+        const int nbox = (a.Hx + kBoxKx - 1) / kBoxKx;
+        const size_t smem = (size_t)(stage_offset<cplx<T>>(PL::slots(d.L)) + 2 * nbox * kBoxKx) * sizeof(cplx<T>) + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd((a.nrows + 1) / 2, a.nslabs);
+        kern<<<grd, PL::NT, smem, st>>>(a, d, imap);
+        return cudaGetLastError();
+      }
+    }
     auto kern = k_row_c2r<PL, Shape<PL>::row_threads, Shape<PL>::row_minb>;
     const int P = row_teams<PL>(kern, d, a.nrows);
     const size_t smem = (size_t)P * PL::slots(d.L) * sizeof(cplx<T>);
@@ -598,7 +989,7 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
           (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
         auto kern = k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
-        const size_t smem = (size_t)(PL::slots(d.L) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
+        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
@@ -627,7 +1018,7 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
         auto kern = k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
-        const size_t smem = (size_t)(PL::slots(d.L) + d.L) * esz + 16;
+        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         dim3 grd(a.Hx, a.nbatch), blk(PL::NT);

@@ -18,8 +18,10 @@ struct RowR2CArgs {
   int ld_out, Hx;
 };
 
-// Transposed half spectra -> real rows.  Input (s, kx, j) at
-// in + s*in_sstride + kx*ld_in + j (j < nrows); output row j, column i < nout at
+// Half spectra -> real rows.  Input (s, kx, j) at in + s*in_sstride +
+// kx*ld_in + j (rowmajor = 0, the column stage's natural [kx][j] layout) or
+// in + s*in_sstride + j*ld_in + kx (rowmajor = 1, contiguous rows); j < nrows.
+// Output row j, column i < nout at
 // out + (s/spb)*out_bstride + (s%spb)*out_sstride + j*ld_out + i.
 struct RowC2RArgs {
   const void* in;
@@ -28,6 +30,7 @@ struct RowC2RArgs {
   void* out;
   long long out_bstride, out_sstride;
   int spb, ld_out, nout;
+  int rowmajor;
 };
 
 // Forward operator, column stage for one chunk of K layers:
@@ -45,7 +48,9 @@ struct ColFwdArgs {
 };
 
 // Transpose operator, column stage for one chunk of K layers:
-// Wt[b][r][kx][q<nout] = IFFT_y( conj(S_r[kx]) * FFT_y(D[b][kx][0:nvalid]) ).
+// Wt[b][r](kx, q<nout) = IFFT_y( conj(S_r[kx]) * FFT_y(D[b][kx][0:nvalid]) ),
+// stored at kx*ldw + q (rowmajor = 0) or q*ldw + kx (rowmajor = 1: the C2R
+// row pass then reads contiguous rows; the transposition is paid by stores).
 struct ColTraArgs {
   const void* D;
   long long d_bstride;
@@ -56,6 +61,7 @@ struct ColTraArgs {
   void* W;
   long long w_bstride, w_rstride;
   int ldw, nout, Hx, nbatch;
+  int rowmajor;
 };
 
 // Spectrum build, column stage: S[kx][ky] = scale * FFT_y(Y[kx][0:Ly]) (fp64 FFT,

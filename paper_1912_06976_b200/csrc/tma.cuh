@@ -64,3 +64,37 @@ __device__ __forceinline__ void tma_load(void* dst_smem, const void* src_gmem, u
 }
 
 }  // namespace bttb
+
+// ---------------------------------------------------------------------------
+// Tensor (2-D/3-D tiled) TMA: used for the transposed [kx][row] tiles of the
+// row passes, where a CTA's rows form a narrow strided box that plain
+// 16-byte stores/loads would scatter over one L2 line per lane.
+// ---------------------------------------------------------------------------
+#include <cuda.h>
+
+namespace bttb {
+
+// store smem -> global box at coordinates (c0, c1, c2) (bulk-group completion)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// wait until the committed stores have finished READING shared memory
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// load global box at (c0, c1, c2) -> smem, completion on an mbarrier
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(smem)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+}  // namespace bttb
