@@ -189,7 +189,7 @@ struct DeviceGuard {
 size_t chunk_budget() {
   const char* env = getenv("BTTB_CHUNK_BYTES");
   if (env) return (size_t)atoll(env);
-  return (size_t)64 << 20;
+  return (size_t)96 << 20;
 }
 
 size_t round_up(size_t n, size_t a) { return (n + a - 1) / a * a; }

@@ -697,9 +697,19 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_spec(ColSpecArgs a, FFTDesc<
 // ---------------------------------------------------------------------------
 template <class P> struct Tag { using type = P; };
 
-template <class T, class F>
+// opt-in (BTTB_COL_E10=1): measured slower on C4 fp64 (9.2 vs 7.7 ms/step) --
+// the third shared-memory exchange costs more than the occupancy it buys
+bool col_e10() {
+  static const bool on = getenv("BTTB_COL_E10") && atoi(getenv("BTTB_COL_E10")) != 0;
+  return on;
+}
+
+// COL selects the plan of the accumulating column kernels where it differs
+// (fp64 L=2000: 10 elements per thread keeps the E-element accumulator cheap)
+template <class T, bool COL = false, class F>
 cudaError_t with_plan(int L, int E, F&& f) {
   if constexpr (sizeof(T) == 8) {
+    if (COL && L == 2000 && col_e10()) return f(Tag<SPlan<double, 10, 40, 10, 10, 10, 2>>{});
     switch (L) {
       case 2048: return f(Tag<SPlan<double, 8, 8, 8, 8, 8, 4>>{});
       case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
@@ -754,7 +764,7 @@ template <class PL> struct Shape {
   }
   // register targets: the column kernels keep E-element accumulators beside the data
   static constexpr int col_regs = 64 + 4 * PL::E * (int)(sizeof(T) / 4) > 255 ? 255 : 64 + 4 * PL::E * (int)(sizeof(T) / 4);
-  static constexpr int col_regs_rounded = col_regs <= 128 ? 128 : (col_regs <= 168 ? 168 : 255);
+  static constexpr int col_regs_rounded = col_regs <= 128 ? 128 : (col_regs <= 144 ? 144 : (col_regs <= 168 ? 168 : 255));
   static constexpr int row_minb = PL::kStatic ? minb(row_threads, 128) : 1;
   // fp64 plans with 20 elements per thread keep the column accumulator in
   // shared memory (registers would cap occupancy at two teams per SM)
@@ -982,7 +992,7 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
 template <class T>
 cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
-  return with_plan<T>(d.L, E, [&](auto tag) {
+  return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
       const size_t esz = sizeof(cplx<T>);
@@ -1012,7 +1022,7 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
 template <class T>
 cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
-  return with_plan<T>(d.L, E, [&](auto tag) {
+  return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
       const size_t esz = sizeof(cplx<T>);
