@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
+                         "(for ncu --profile-from-start off); prints nothing")
     return ap.parse_args()
 
 
@@ -252,6 +255,14 @@ def run_ours(a):
     for _ in range(max(3, a.warmup)):
         step()
     barrier()
+    if a.profile_step:
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        if world > 1:
+            dist.destroy_process_group()
+        return
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.15)
