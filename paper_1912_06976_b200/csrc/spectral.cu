@@ -573,15 +573,29 @@ template <class V> __host__ __device__ __forceinline__ int stage_offset(int slot
   return (slots + per - 1) / per * per;
 }
 
+// The staging tile lives in the exchange buffer itself: the separated values
+// are first gathered into the registers the finished FFT no longer needs,
+// then written as the [kx][2 rows] box -> one team buffer per CTA (36 KB for
+// fp64 L=2000), four CTAs per SM.
+template <class PL> struct RowTile {
+  static constexpr int HX = PL::L / 2 + 1;
+  static constexpr int NI = (HX + PL::NT - 1) / PL::NT;  // kx items per thread
+  static constexpr int NBOX = (HX + kBoxKx - 1) / kBoxKx;
+  // shared slots (complex) of one CTA: exchange buffer or staged box, whichever is larger
+  static constexpr int slots(int exchange_slots) {
+    return exchange_slots > 2 * NBOX * kBoxKx ? exchange_slots : 2 * NBOX * kBoxKx;
+  }
+};
+
 template <class PL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_r2c_t2d(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap omap) {
   using T = typename PL::Scalar;
   using V = cplx<T>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  using RT = RowTile<PL>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* sm = reinterpret_cast<V*>(smraw);
-  V* stage = sm + stage_offset<V>(PL::slots(L));
   const int t = threadIdx.x, s = blockIdx.y, qa = 2 * blockIdx.x, qb = qa + 1;
   const T* in = static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride +
                 (long long)(s % a.spb) * a.in_sstride;
@@ -601,16 +615,30 @@ __global__ void __launch_bounds__(MAXT, MINB)
   for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
   __syncthreads();
   const T h = T(0.5);
-  for (int kx = t; kx < a.Hx; kx += NT) {
-    const V zk = sm[PL::slot(kx)];
-    const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
-    stage[2 * kx] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
-    stage[2 * kx + 1] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+  V A[NI], B[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int kx = t + NT * i;
+    if (kx < HX) {
+      const V zk = sm[PL::slot(kx)];
+      const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
+      A[i] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
+      B[i] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int kx = t + NT * i;
+    if (kx < HX) {
+      sm[2 * kx] = A[i];
+      sm[2 * kx + 1] = B[i];
+    }
   }
   fence_proxy_async();
   __syncthreads();
   if (t == 0) {
-    for (int kx0 = 0; kx0 < a.Hx; kx0 += kBoxKx) tma_store_3d(&omap, stage + 2 * kx0, 2 * qa, kx0, s);
+    for (int kx0 = 0; kx0 < HX; kx0 += kBoxKx) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
     tma_store_commit();
     tma_store_wait_read();
   }
@@ -621,29 +649,42 @@ __global__ void __launch_bounds__(MAXT, MINB)
     k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
   using T = typename PL::Scalar;
   using V = cplx<T>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  using RT = RowTile<PL>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI, NBOX = RT::NBOX;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* sm = reinterpret_cast<V*>(smraw);
-  V* stage = sm + stage_offset<V>(PL::slots(L));
-  const int nbox = (a.Hx + kBoxKx - 1) / kBoxKx;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + 2 * nbox * kBoxKx);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + RT::slots((PL::slots(L) + 1) & ~1));
   const int t = threadIdx.x, s = blockIdx.y, ja = 2 * blockIdx.x, jb = ja + 1;
   if (t == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(bar, (uint32_t)(nbox * kBoxKx * 2 * sizeof(V)));
-    for (int b = 0; b < nbox; ++b) tma_load_3d(stage + 2 * b * kBoxKx, &imap, 2 * ja, b * kBoxKx, s, bar);
+    mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * kBoxKx * 2 * sizeof(V)));
+    for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * kBoxKx, &imap, 2 * ja, b * kBoxKx, s, bar);
   }
   __syncthreads();
   mbar_wait(bar, 0);
-  for (int kx = t; kx < a.Hx; kx += NT) {
-    V A = stage[2 * kx], B = stage[2 * kx + 1];  // out-of-range rows arrive zero-filled
-    if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
-      A.y = T(0);
-      B.y = T(0);
+  V A[NI], B[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int kx = t + NT * i;
+    if (kx < HX) {
+      A[i] = sm[2 * kx];  // out-of-range rows arrive zero-filled
+      B[i] = sm[2 * kx + 1];
     }
-    sm[PL::slot(kx)] = mkc<V>(A.x - B.y, A.y + B.x);
-    if (kx >= 1 && kx <= L - a.Hx) sm[PL::slot(L - kx)] = mkc<V>(A.x + B.y, B.x - A.y);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int kx = t + NT * i;
+    if (kx < HX) {
+      V a0 = A[i], b0 = B[i];
+      if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
+        a0.y = T(0);
+        b0.y = T(0);
+      }
+      sm[PL::slot(kx)] = mkc<V>(a0.x - b0.y, a0.y + b0.x);
+      if (kx >= 1 && kx <= L - HX) sm[PL::slot(L - kx)] = mkc<V>(a0.x + b0.y, b0.x - a0.y);
+    }
   }
   __syncthreads();
   V v[E];
@@ -928,7 +969,7 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
       if (t2d_ok() && a.Hx <= 65535 &&
           encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride)) {
         auto kern = k_row_r2c_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
-        const size_t smem = (size_t)(stage_offset<cplx<T>>(PL::slots(d.L)) + 2 * a.Hx) * sizeof(cplx<T>);
+        const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         dim3 grd((a.nrows + 1) / 2, a.nslabs);
@@ -969,8 +1010,7 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
       if (t2d_ok() && !a.rowmajor &&
           encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride)) {
         auto kern = k_row_c2r_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
-        const int nbox = (a.Hx + kBoxKx - 1) / kBoxKx;
-        const size_t smem = (size_t)(stage_offset<cplx<T>>(PL::slots(d.L)) + 2 * nbox * kBoxKx) * sizeof(cplx<T>) + 16;
+        const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         dim3 grd((a.nrows + 1) / 2, a.nslabs);
