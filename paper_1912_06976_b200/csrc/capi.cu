@@ -194,6 +194,13 @@ size_t chunk_budget() {
 
 size_t round_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
 
+// overlap the row pass of chunk c+1 with the column stage of chunk c on two
+// streams (double-buffered chunk workspace); opt-in with BTTB_PIPELINE=1
+bool pipelined() {
+  static const bool on = getenv("BTTB_PIPELINE") && atoi(getenv("BTTB_PIPELINE")) != 0;  // measured slower: 8.66 vs 7.16 ms
+  return on;
+}
+
 // transpose intermediate layout: row-major [q][kx] (BTTB_TRA_ROWMAJOR=1) or [kx][q]
 bool tra_rowmajor() {
   static const bool rm = getenv("BTTB_TRA_ROWMAJOR") && atoi(getenv("BTTB_TRA_ROWMAJOR")) != 0;
@@ -214,8 +221,10 @@ struct bttb_plan_s {
   size_t elem = 16;
   void* spectra = nullptr;
   DevBuf work, hin, hout;
-  cudaStream_t stream = nullptr;  // internal stream carrying the L2 persisting window
+  cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
+  cudaStream_t stream2 = nullptr;  // second stream: column stages, overlapped with the next chunk's row pass
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_row[2] = {nullptr, nullptr}, ev_col[2] = {nullptr, nullptr}, ev_aux = nullptr;
   void* window_base = nullptr;
   size_t window_bytes = 0;
   int64_t last_K = 0, last_G = 0, last_launches = 0;
@@ -397,6 +406,7 @@ int set_l2_window(bttb_plan_s* p, void* base, size_t bytes) {
   v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
   v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
   CU(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  CU(cudaStreamSetAttribute(p->stream2, cudaStreamAttributeAccessPolicyWindow, &v));
   p->window_base = base;
   p->window_bytes = bytes;
   return BTTB_OK;
@@ -415,25 +425,36 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
   int64_t G = 1;
   if (K == p->nzl) G = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(budget / (slab * p->nzl))));
   int rc;
-  // one workspace: the chunk intermediate Y (row-pass output / transposed
-  // column output) then the accumulator / data half-spectrum W; both are kept
-  // L2-resident by the persisting access-policy window on the plan's stream
+  // workspace: two chunk intermediates Y[0..1] (row-pass output / transposed
+  // column output; double-buffered so chunk c+1's row pass overlaps chunk c's
+  // column stage) then the accumulator / data half-spectrum W
+  const bool pipe = pipelined();
+  const int nbuf = pipe ? 2 : 1;
   const size_t ybytes = round_up(slab * K * G, 4096), wbytes = round_up((size_t)Hx * sy * sizeof(V) * G, 4096);
-  if ((rc = p->work.ensure(ybytes + wbytes))) return rc;
-  if ((rc = set_l2_window(p, p->work.p, ybytes + wbytes))) return rc;
+  if ((rc = p->work.ensure(nbuf * ybytes + wbytes))) return rc;
+  if ((rc = set_l2_window(p, p->work.p, nbuf * ybytes + wbytes))) return rc;
   p->last_K = K;
   p->last_G = G;
   int64_t launches = 0;
-  V* Yb = static_cast<V*>(p->work.p);
-  V* Wb = reinterpret_cast<V*>(static_cast<char*>(p->work.p) + ybytes);
+  V* Ybuf[2] = {static_cast<V*>(p->work.p), reinterpret_cast<V*>(static_cast<char*>(p->work.p) + (pipe ? ybytes : 0))};
+  V* Wb = reinterpret_cast<V*>(static_cast<char*>(p->work.p) + nbuf * ybytes);
   const V* S = static_cast<const V*>(p->spectra);
   const long long s_rstride = (long long)Hx * p->Ly;
+  cudaStream_t sa = st, sb = pipe ? p->stream2 : st;  // sa: row passes, sb: column stages
+  if (pipe) {
+    CU(cudaEventRecord(p->ev_aux, sa));  // sb starts after everything already ordered on sa
+    CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
+  }
+  int chunk = 0;
   for (int64_t b0 = 0; b0 < batch; b0 += G) {
     const int gb = (int)std::min<int64_t>(G, batch - b0);
     if (mode == BTTB_FORWARD) {
       const T* xin = static_cast<const T*>(x) + b0 * nloc;
-      for (int64_t r0 = 0; r0 < p->nzl; r0 += K) {
+      for (int64_t r0 = 0; r0 < p->nzl; r0 += K, ++chunk) {
         const int k = (int)std::min<int64_t>(K, p->nzl - r0);
+        const int bi = chunk % nbuf;
+        V* Yb = Ybuf[bi];
+        if (pipe) CU(cudaStreamWaitEvent(sa, p->ev_col[bi], 0));  // column stage of chunk-2 done with Yb
         RowR2CArgs ra{};
         ra.in = xin + r0 * n_r;
         ra.in_bstride = nloc;
@@ -447,7 +468,11 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ra.out_sstride = (long long)Hx * ny;
         ra.ld_out = (int)ny;
         ra.Hx = (int)Hx;
-        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
+        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), sa));
+        if (pipe) {
+          CU(cudaEventRecord(p->ev_row[bi], sa));
+          CU(cudaStreamWaitEvent(sb, p->ev_row[bi], 0));
+        }
         ColFwdArgs ca{};
         ca.Y = Yb;
         ca.y_bstride = (long long)k * Hx * ny;
@@ -465,8 +490,13 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.accumulate = r0 > 0;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
-        CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), st));
+        CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), sb));
+        if (pipe) CU(cudaEventRecord(p->ev_col[bi], sb));
         launches += 2;
+      }
+      if (pipe) {
+        CU(cudaEventRecord(p->ev_aux, sb));
+        CU(cudaStreamWaitEvent(sa, p->ev_aux, 0));
       }
       RowC2RArgs oa{};
       oa.in = Wb;
@@ -481,8 +511,12 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       oa.spb = 1;
       oa.ld_out = (int)sx;
       oa.nout = (int)sx;
-      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
+      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), sa));
       launches += 1;
+      if (pipe) {  // the next batch group's column stages must not overwrite W early
+        CU(cudaEventRecord(p->ev_aux, sa));
+        CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
+      }
     } else {
       RowR2CArgs ra{};
       ra.in = static_cast<const T*>(x) + b0 * m;
@@ -497,11 +531,18 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       ra.out_sstride = (long long)Hx * sy;
       ra.ld_out = (int)sy;
       ra.Hx = (int)Hx;
-      CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
+      CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), sa));
       launches += 1;
+      if (pipe) {
+        CU(cudaEventRecord(p->ev_aux, sa));
+        CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
+      }
       T* yout = static_cast<T*>(y) + b0 * nloc;
-      for (int64_t r0 = 0; r0 < p->nzl; r0 += K) {
+      for (int64_t r0 = 0; r0 < p->nzl; r0 += K, ++chunk) {
         const int k = (int)std::min<int64_t>(K, p->nzl - r0);
+        const int bi = chunk % nbuf;
+        V* Yb = Ybuf[bi];
+        if (pipe) CU(cudaStreamWaitEvent(sb, p->ev_row[bi], 0));  // row pass of chunk-2 done reading Yb
         ColTraArgs ca{};
         ca.D = Wb;
         ca.d_bstride = (long long)Hx * sy;
@@ -519,7 +560,11 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.nout = (int)ny;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
-        CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), st));
+        CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), sb));
+        if (pipe) {
+          CU(cudaEventRecord(p->ev_col[bi], sb));
+          CU(cudaStreamWaitEvent(sa, p->ev_col[bi], 0));
+        }
         RowC2RArgs oa{};
         oa.in = Yb;
         oa.in_sstride = (long long)Hxp * ny;
@@ -534,8 +579,13 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         oa.ld_out = (int)nx;
         oa.nout = (int)nx;
         oa.rowmajor = ca.rowmajor;
-        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
+        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), sa));
+        if (pipe) CU(cudaEventRecord(p->ev_row[bi], sa));
         launches += 2;
+      }
+      if (pipe) {  // W (the data half-spectrum) is rewritten by the next batch group's row pass on sa
+        CU(cudaEventRecord(p->ev_aux, sb));
+        CU(cudaStreamWaitEvent(sa, p->ev_aux, 0));
       }
     }
   }
@@ -551,6 +601,12 @@ void destroy_plan(bttb_plan_s* p) {
   p->fy.release();
   p->work.release();
   if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->stream2) cudaStreamDestroy(p->stream2);
+  for (int i = 0; i < 2; ++i) {
+    if (p->ev_row[i]) cudaEventDestroy(p->ev_row[i]);
+    if (p->ev_col[i]) cudaEventDestroy(p->ev_col[i]);
+  }
+  if (p->ev_aux) cudaEventDestroy(p->ev_aux);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   p->hin.release();
@@ -634,10 +690,15 @@ int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* 
     }
   }
   if (!rc) {
-    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) != cudaSuccess)
-      rc = fail(BTTB_ECUDA, "cannot create the plan stream");
+    bool ok = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_aux, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; ++i)
+      ok = cudaEventCreateWithFlags(&p->ev_row[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) rc = fail(BTTB_ECUDA, "cannot create the plan streams/events");
   }
   if (!rc) rc = build_spectra(p);
   if (rc) {

@@ -644,6 +644,97 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
 }
 
+// Persistent R2C: each CTA walks row pairs with a stride of gridDim.x; thread 0
+// bulk-copies the NEXT pair's two rows into a row stage while the team
+// transforms the current pair, then the tile leaves by tensor-TMA store.
+// Shared: [exchange/stage tile (RowTile::slots)][row stage 2 x rowcap reals][mbarrier].
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+    k_row_r2c_pt(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap omap, int rowcap) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  using RT = RowTile<PL>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* sm = reinterpret_cast<V*>(smraw);
+  T* rows = reinterpret_cast<T*>(sm + RT::slots((PL::slots(L) + 1) & ~1));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rows + 2 * rowcap);
+  const int t = threadIdx.x;
+  const int npairs = (a.nrows + 1) / 2, total = npairs * a.nslabs;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t bytes = a.nvalid * sizeof(T);
+  auto row_ptr = [&](int item, int which) {
+    const int s = item / npairs, q = 2 * (item - s * npairs) + which;
+    return static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride + (long long)(s % a.spb) * a.in_sstride +
+           (long long)q * a.ld_in;
+  };
+  auto has_b = [&](int item) { return 2 * (item % npairs) + 1 < a.nrows; };
+  auto issue = [&](int item) {
+    const bool b2 = has_b(item);
+    mbar_arrive_expect_tx(bar, b2 ? 2 * bytes : bytes);
+    tma_load(rows, row_ptr(item, 0), bytes, bar, pol);
+    if (b2) tma_load(rows + rowcap, row_ptr(item, 1), bytes, bar, pol);
+  };
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    if ((int)blockIdx.x < total) issue(blockIdx.x);
+  }
+  __syncthreads();
+  const T h = T(0.5);
+  int it = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+    mbar_wait(bar, it & 1);
+    const bool vb = has_b(item);
+    V v[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int i = t + NT * k;
+      const bool inb = i < a.nvalid;
+      v[k] = mkc<V>(inb ? rows[i] : T(0), inb && vb ? rows[rowcap + i] : T(0));
+    }
+    __syncthreads();  // rows consumed; also orders the previous tile's TMA store read (below)
+    if (t == 0 && item + (int)gridDim.x < total) {
+      fence_proxy_async();
+      issue(item + gridDim.x);
+    }
+    PL::fft(v, sm, t, d);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
+    __syncthreads();
+    V A[NI], B[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int kx = t + NT * i;
+      if (kx < HX) {
+        const V zk = sm[PL::slot(kx)];
+        const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
+        A[i] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
+        B[i] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int kx = t + NT * i;
+      if (kx < HX) {
+        sm[2 * kx] = A[i];
+        sm[2 * kx + 1] = B[i];
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (t == 0) {
+      const int s = item / npairs, qa = 2 * (item - s * npairs);
+      for (int kx0 = 0; kx0 < HX; kx0 += kBoxKx) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
+      tma_store_commit();
+      tma_store_wait_read();  // the tile region is the next FFT's exchange buffer
+    }
+    __syncthreads();
+  }
+}
+
 template <class PL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
@@ -904,6 +995,11 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+bool persistent_r2c() {
+  static const bool on = getenv("BTTB_R2C_PERSIST") && atoi(getenv("BTTB_R2C_PERSIST")) != 0;  // measured slower (7.61 vs 7.26 ms)
+  return on;
+}
+
 bool t2d_ok() {
   static const bool ok = tma_ok() && encode_fn() != nullptr && !(getenv("BTTB_T2D") && atoi(getenv("BTTB_T2D")) == 0);
   return ok;
@@ -968,6 +1064,19 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
       CUtensorMap omap;
       if (t2d_ok() && a.Hx <= 65535 &&
           encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride)) {
+        const size_t esz = sizeof(T);
+        if (persistent_r2c() && al16(a.in) && (a.nvalid * esz) % 16 == 0 && (a.ld_in * esz) % 16 == 0 &&
+            (a.in_sstride * esz) % 16 == 0 && (a.in_bstride * esz) % 16 == 0) {
+          auto kern = k_row_r2c_pt<PL, PL::NT, Shape<PL>::t2d_minb>;
+          const int rowcap = (a.nvalid + 3) & ~3;
+          const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) +
+                              2 * (size_t)rowcap * esz + 16;
+          cudaError_t e = set_smem(kern, smem);
+          if (e != cudaSuccess) return e;
+          const int items = (a.nrows + 1) / 2 * a.nslabs;
+          kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, omap, rowcap);
+          return cudaGetLastError();
+        }
         auto kern = k_row_r2c_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
         const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
         cudaError_t e = set_smem(kern, smem);
