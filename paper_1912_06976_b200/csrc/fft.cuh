@@ -307,29 +307,36 @@ __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx
 }
 
 template <class T, int E, int R, int NS, int NT, int PAD>
-__device__ __forceinline__ void spass_store(const cplx<T> (&v)[E], cplx<T>* sm, int t) {
+__device__ __forceinline__ void spass_store(const cplx<T> (&v)[E], cplx<T>* sm, int t, bool active = true) {
   constexpr int NB = E / R;
   sfor<0, NB>([&](auto bc) {
     constexpr int b = decltype(bc)::value;
     const int j = t + NT * b;
     const int k = j % NS;
     const int base = (j - k) * R + k;
-    sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; sm[pad_slot<PAD>(base + r * NS)] = v[b + r * NB]; });
+    sfor<0, R>([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      if (active) sm[pad_slot<PAD>(base + r * NS)] = v[b + r * NB];
+    });
   });
 }
 
+// `active` = false: the thread follows the same control flow and barriers but
+// touches no shared memory (helper lanes that pad a team to whole warps).
 template <class T, int E, int L, int PAD, int NS, int R, int... Rest>
-__device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw) {
+__device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
+                                     bool active = true) {
   constexpr int NT = L / E;
   static_assert(E % R == 0, "radix must divide elements per thread");
-  spass_compute<T, E, R, NS, NT, L>(v, t, tw);
+  spass_compute<T, E, R, NS, NT, L>(v, active ? t : 0, tw);
   if constexpr (sizeof...(Rest) > 0) {
     __syncthreads();
-    spass_store<T, E, R, NS, NT, PAD>(v, sm, t);
+    spass_store<T, E, R, NS, NT, PAD>(v, sm, t, active);
     __syncthreads();
 #pragma unroll
-    for (int s = 0; s < E; ++s) v[s] = sm[pad_slot<PAD>(t + NT * s)];
-    sfft<T, E, L, PAD, NS * R, Rest...>(v, sm, t, tw);
+    for (int s = 0; s < E; ++s)
+      if (active) v[s] = sm[pad_slot<PAD>(t + NT * s)];
+    sfft<T, E, L, PAD, NS * R, Rest...>(v, sm, t, tw, active);
   }
 }
 
@@ -348,6 +355,10 @@ struct SPlan {
   __host__ __device__ __forceinline__ static int slots(int len) { return pad_slot<PAD>(len) + 1; }
   __device__ __forceinline__ static void fft(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d) {
     sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw);
+  }
+  __device__ __forceinline__ static void fft_masked(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
+                                                    bool active) {
+    sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw, active);
   }
 };
 

@@ -25,6 +25,10 @@
 #include "spectral.h"
 #include "tma.cuh"
 
+#ifndef T2D_TEAMS
+#define T2D_TEAMS 1  // row pairs (teams) per CTA of the tensor-TMA row passes
+#endif
+
 namespace bttb {
 
 namespace {
@@ -402,6 +406,216 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
 }
 
 // ---------------------------------------------------------------------------
+// TMEM variants of the TMA column stages (fp64 plans whose team is not a whole
+// number of warps, e.g. L=2000: 100 threads).  The per-thread E-element
+// accumulator (forward) or data spectrum (transpose) -- 80 registers in fp64
+// -- lives in tensor memory, which this workload otherwise leaves idle; the
+// CTA is padded to whole warps (helper lanes follow the control flow and
+// barriers, touch no shared memory) as tcgen05 ld/st are warp-collective.
+// With registers freed and the Y column loaded straight from global, three
+// CTAs fit per SM instead of two.  Shared: [exchange][spectrum L][mbarrier][tmem addr].
+// ---------------------------------------------------------------------------
+template <class PL> struct TmemCfg {
+  static constexpr int NTR = (PL::NT + 31) / 32 * 32;
+  static constexpr int COLS = PL::E * 4;  // fp64 complex = 4 x 32-bit columns
+  static constexpr int GROUPS = COLS / 16;
+  static constexpr int NCOLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
+  static_assert(COLS % 16 == 0, "TMEM groups of 16 columns = 4 complex");
+};
+
+__device__ __forceinline__ void split4(double2 a, uint32_t* r) {
+  r[0] = (uint32_t)__double2loint(a.x);
+  r[1] = (uint32_t)__double2hiint(a.x);
+  r[2] = (uint32_t)__double2loint(a.y);
+  r[3] = (uint32_t)__double2hiint(a.y);
+}
+__device__ __forceinline__ double2 join4(const uint32_t* r) {
+  return make_double2(__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2]));
+}
+
+template <class PL, int MINB>
+__global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_fwd_tmem(ColFwdArgs a, FFTDesc<double> d) {
+  using V = double2;
+  using TC = TmemCfg<PL>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = (PL::slots(L) + 1) & ~1;
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* sbuf = sm + Ls;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + L);
+  uint32_t* taddr_s = reinterpret_cast<uint32_t*>(bar + 1);
+  const int t = threadIdx.x, warp = t / 32;
+  const bool active = t < NT;
+  const int kx = blockIdx.x, b = blockIdx.y;
+  const uint32_t sbytes = L * sizeof(V);
+  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const uint64_t pol = policy_evict_first();
+  if (warp == 0) tmem_alloc<TC::NCOLS>(taddr_s);
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, sbytes);
+    tma_load(sbuf, Sb, sbytes, bar, pol);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t ta = *taddr_s + ((uint32_t)(32 * (warp & 3)) << 16);
+  {
+    uint32_t z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll
+    for (int g = 0; g < TC::GROUPS; ++g) tmem_st16(ta + 16 * g, z);
+    tmem_wait_st();
+  }
+  V v[E];
+  for (int r = 0; r < a.K; ++r) {
+    const V* yc = Yb + (long long)r * a.y_rstride;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int q = t + NT * k;
+      v[k] = active && q < a.nvalid ? yc[q] : mkc<V>(0.0, 0.0);
+    }
+    PL::fft_masked(v, sm, t, d, active);
+    mbar_wait(bar, r & 1);
+#pragma unroll
+    for (int g = 0; g < TC::GROUPS; ++g) {
+      uint32_t acc[16];
+      tmem_ld16(ta + 16 * g, acc);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int k = 4 * g + c;
+        V o = join4(acc + 4 * c);
+        const V w = active ? sbuf[t + NT * k] : mkc<V>(0.0, 0.0);
+        o.x += w.x * v[k].x - w.y * v[k].y;
+        o.y += w.x * v[k].y + w.y * v[k].x;
+        split4(o, acc + 4 * c);
+      }
+      tmem_st16(ta + 16 * g, acc);
+    }
+    tmem_wait_st();
+    __syncthreads();
+    if (t == 0 && r + 1 < a.K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, sbytes);
+      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, bar, pol);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < TC::GROUPS; ++g) {
+    uint32_t acc[16];
+    tmem_ld16(ta + 16 * g, acc);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[4 * g + c] = conjv(join4(acc + 4 * c));
+  }
+  PL::fft_masked(v, sm, t, d, active);
+  if (active) {
+    V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int j = t + NT * k;
+      if (j < a.nout) {
+        V val = conjv(v[k]);
+        if (a.accumulate) val = val + wc[j];
+        wc[j] = val;
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<TC::NCOLS>(*taddr_s);
+}
+
+template <class PL, int MINB>
+__global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_tra_tmem(ColTraArgs a, FFTDesc<double> d) {
+  using V = double2;
+  using TC = TmemCfg<PL>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = (PL::slots(L) + 1) & ~1;
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* sbuf = sm + Ls;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + L);
+  uint32_t* taddr_s = reinterpret_cast<uint32_t*>(bar + 1);
+  const int t = threadIdx.x, warp = t / 32;
+  const bool active = t < NT;
+  const int kx = blockIdx.x, b = blockIdx.y;
+  const uint32_t sbytes = L * sizeof(V);
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const uint64_t pol = policy_evict_first();
+  if (warp == 0) tmem_alloc<TC::NCOLS>(taddr_s);
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, sbytes);
+    tma_load(sbuf, Sb, sbytes, bar, pol);
+  }
+  V v[E];
+  const V* dc = static_cast<const V*>(a.D) + (long long)b * a.d_bstride + (long long)kx * a.ldd;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int j = t + NT * k;
+    v[k] = active && j < a.nvalid ? dc[j] : mkc<V>(0.0, 0.0);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t ta = *taddr_s + ((uint32_t)(32 * (warp & 3)) << 16);
+  PL::fft_masked(v, sm, t, d, active);
+#pragma unroll
+  for (int g = 0; g < TC::GROUPS; ++g) {  // the data spectrum, read once per layer below
+    uint32_t u[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) split4(v[4 * g + c], u + 4 * c);
+    tmem_st16(ta + 16 * g, u);
+  }
+  tmem_wait_st();
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw);
+  const long long qstride = a.rowmajor ? a.ldw : 1;
+  for (int r = 0; r < a.K; ++r) {
+    mbar_wait(bar, r & 1);
+#pragma unroll
+    for (int g = 0; g < TC::GROUPS; ++g) {
+      uint32_t u[16];
+      tmem_ld16(ta + 16 * g, u);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int k = 4 * g + c;
+        const V h = join4(u + 4 * c);
+        // conj(conj(S) * dh) = S * conj(dh): inverse FFT via the conjugation identity
+        const V w = active ? sbuf[t + NT * k] : mkc<V>(0.0, 0.0);
+        v[k] = mkc<V>(w.x * h.x + w.y * h.y, w.y * h.x - w.x * h.y);
+      }
+    }
+    __syncthreads();
+    if (t == 0 && r + 1 < a.K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, sbytes);
+      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, bar, pol);
+    }
+    PL::fft_masked(v, sm, t, d, active);
+    if (active) {
+      V* wc = Wb + (long long)r * a.w_rstride;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const int q = t + NT * k;
+        if (q < a.nout) wc[q * qstride] = conjv(v[k]);
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<TC::NCOLS>(*taddr_s);
+}
+
+// ---------------------------------------------------------------------------
 // Persistent, TMA double-buffered row passes (compile-time plans, one row pair
 // per iteration, one team per CTA).  Thread 0 bulk-copies the rows of the pair
 // two iterations ahead into the stage just consumed, so the contiguous row
@@ -581,13 +795,16 @@ template <class PL> struct RowTile {
   static constexpr int HX = PL::L / 2 + 1;
   static constexpr int NI = (HX + PL::NT - 1) / PL::NT;  // kx items per thread
   static constexpr int NBOX = (HX + kBoxKx - 1) / kBoxKx;
-  // shared slots (complex) of one CTA: exchange buffer or staged box, whichever is larger
+  // shared slots (complex) of one team: exchange buffer or staged box, whichever
+  // is larger, rounded to 128 bytes (tensor-TMA shared addresses are 128-B aligned)
   static constexpr int slots(int exchange_slots) {
-    return exchange_slots > 2 * NBOX * kBoxKx ? exchange_slots : 2 * NBOX * kBoxKx;
+    constexpr int per = 128 / (int)sizeof(cplx<typename PL::Scalar>);
+    const int n = exchange_slots > 2 * NBOX * kBoxKx ? exchange_slots : 2 * NBOX * kBoxKx;
+    return (n + per - 1) / per * per;
   }
 };
 
-template <class PL, int MAXT, int MINB>
+template <class PL, int MAXT, int MINB, int TEAMS>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_r2c_t2d(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap omap) {
   using T = typename PL::Scalar;
@@ -595,19 +812,21 @@ __global__ void __launch_bounds__(MAXT, MINB)
   using RT = RowTile<PL>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI;
   extern __shared__ __align__(16) unsigned char smraw[];
-  V* sm = reinterpret_cast<V*>(smraw);
-  const int t = threadIdx.x, s = blockIdx.y, qa = 2 * blockIdx.x, qb = qa + 1;
+  const int c = TEAMS > 1 ? threadIdx.x / NT : 0;
+  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * RT::slots((PL::slots(L) + 1) & ~1);
+  const int t = threadIdx.x - c * NT, s = blockIdx.y, qa = 2 * (blockIdx.x * TEAMS + c), qb = qa + 1;
+  const bool active = qa < a.nrows;
   const T* in = static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride +
                 (long long)(s % a.spb) * a.in_sstride;
   const bool vb = qb < a.nrows;
-  const T* ra = in + (long long)qa * a.ld_in;
+  const T* ra = in + (long long)(active ? qa : 0) * a.ld_in;
   const T* rb = in + (long long)(vb ? qb : qa) * a.ld_in;
   V v[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int i = t + NT * k;
     const bool inb = i < a.nvalid;
-    v[k] = mkc<V>(inb ? __ldcs(ra + i) : T(0), vb && inb ? __ldcs(rb + i) : T(0));
+    v[k] = mkc<V>(active && inb ? __ldcs(ra + i) : T(0), vb && inb ? __ldcs(rb + i) : T(0));
   }
   PL::fft(v, sm, t, d);
   __syncthreads();
@@ -637,7 +856,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
   fence_proxy_async();
   __syncthreads();
-  if (t == 0) {
+  if (t == 0 && active) {
     for (int kx0 = 0; kx0 < HX; kx0 += kBoxKx) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
     tma_store_commit();
     tma_store_wait_read();
@@ -735,7 +954,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
 }
 
-template <class PL, int MAXT, int MINB>
+template <class PL, int MAXT, int MINB, int TEAMS>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
   using T = typename PL::Scalar;
@@ -743,17 +962,20 @@ __global__ void __launch_bounds__(MAXT, MINB)
   using RT = RowTile<PL>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI, NBOX = RT::NBOX;
   extern __shared__ __align__(16) unsigned char smraw[];
-  V* sm = reinterpret_cast<V*>(smraw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + RT::slots((PL::slots(L) + 1) & ~1));
-  const int t = threadIdx.x, s = blockIdx.y, ja = 2 * blockIdx.x, jb = ja + 1;
-  if (t == 0) {
+  const int tslots = RT::slots((PL::slots(L) + 1) & ~1);
+  const int c = TEAMS > 1 ? threadIdx.x / NT : 0;
+  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * tslots;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots) + c;
+  const int t = threadIdx.x - c * NT, s = blockIdx.y, ja = 2 * (blockIdx.x * TEAMS + c), jb = ja + 1;
+  const bool active = ja < a.nrows;
+  if (t == 0 && active) {
     mbar_init(bar, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * kBoxKx * 2 * sizeof(V)));
     for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * kBoxKx, &imap, 2 * ja, b * kBoxKx, s, bar);
   }
   __syncthreads();
-  mbar_wait(bar, 0);
+  if (active) mbar_wait(bar, 0);
   V A[NI], B[NI];
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
@@ -784,12 +1006,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
   PL::fft(v, sm, t, d);
   const bool vb = jb < a.nrows;
   T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
-  T* oa = out + (long long)ja * a.ld_out;
+  T* oa = out + (long long)(active ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int i = t + NT * k;
-    if (i < a.nout) {
+    if (i < a.nout && active) {
       __stcs(oa + i, v[k].x);
       if (vb) __stcs(ob + i, -v[k].y);
     }
@@ -905,7 +1127,8 @@ template <class PL> struct Shape {
   static constexpr int spec_minb = PL::kStatic ? minb(col_threads, 128) : 1;
   static constexpr int tma_minb = PL::kStatic ? minb(col_threads, col_regs_rounded) : 1;
   static constexpr int rowtma_minb = PL::kStatic ? minb(NT, 128) : 1;
-  static constexpr int t2d_minb = PL::kStatic ? minb(NT, 128) : 1;
+  static constexpr int t2d_teams = T2D_TEAMS;
+  static constexpr int t2d_minb = PL::kStatic ? minb(T2D_TEAMS * NT, 128) : 1;
 };
 
 bool tma_ok() {
@@ -995,6 +1218,13 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+// TMEM-resident column accumulators: opt-in (BTTB_TMEM=1); correct, but
+// measured slower on C4 fp64 (7.72 vs 7.21 ms/step)
+bool tmem_ok() {
+  static const bool on = getenv("BTTB_TMEM") && atoi(getenv("BTTB_TMEM")) != 0;
+  return on;
+}
+
 bool persistent_r2c() {
   static const bool on = getenv("BTTB_R2C_PERSIST") && atoi(getenv("BTTB_R2C_PERSIST")) != 0;  // measured slower (7.61 vs 7.26 ms)
   return on;
@@ -1077,12 +1307,13 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
           kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, omap, rowcap);
           return cudaGetLastError();
         }
-        auto kern = k_row_r2c_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
-        const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
+        constexpr int TM = Shape<PL>::t2d_teams;
+        auto kern = k_row_r2c_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM>;
+        const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        dim3 grd((a.nrows + 1) / 2, a.nslabs);
-        kern<<<grd, PL::NT, smem, st>>>(a, d, omap);
+        dim3 grd(((a.nrows + 1) / 2 + TM - 1) / TM, a.nslabs);
+        kern<<<grd, TM * PL::NT, smem, st>>>(a, d, omap);
         return cudaGetLastError();
       }
     }
@@ -1118,12 +1349,13 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
       CUtensorMap imap;
       if (t2d_ok() && !a.rowmajor &&
           encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride)) {
-        auto kern = k_row_c2r_t2d<PL, PL::NT, Shape<PL>::t2d_minb>;
-        const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16;
+        constexpr int TM = Shape<PL>::t2d_teams;
+        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM>;
+        const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        dim3 grd((a.nrows + 1) / 2, a.nslabs);
-        kern<<<grd, PL::NT, smem, st>>>(a, d, imap);
+        dim3 grd(((a.nrows + 1) / 2 + TM - 1) / TM, a.nslabs);
+        kern<<<grd, TM * PL::NT, smem, st>>>(a, d, imap);
         return cudaGetLastError();
       }
     }
@@ -1143,6 +1375,18 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
+    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
+                  (PL::E * 4) % 16 == 0) {
+      if (tma_ok() && tmem_ok() && (a.lds * 16) % 16 == 0 && (a.s_rstride * 16) % 16 == 0) {
+        auto kern = k_col_fwd_tmem<PL, 3>;
+        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * 16 + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd(a.Hx, a.nbatch), blk(TmemCfg<PL>::NTR);
+        kern<<<grd, blk, smem, st>>>(a, d);
+        return cudaGetLastError();
+      }
+    }
     if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
@@ -1173,6 +1417,18 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
+    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
+                  (PL::E * 4) % 16 == 0) {
+      if (tma_ok() && tmem_ok()) {
+        auto kern = k_col_tra_tmem<PL, 3>;
+        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * 16 + 16;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd(a.Hx, a.nbatch), blk(TmemCfg<PL>::NTR);
+        kern<<<grd, blk, smem, st>>>(a, d);
+        return cudaGetLastError();
+      }
+    }
     if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {

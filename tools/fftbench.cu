@@ -111,24 +111,9 @@ void run(int L, const int* radices, int npass, int ncols, int C, int reps) {
 int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 20;
   const int r20[] = {20, 20, 5};
-  const int r16[] = {16, 16, 8};
-  const int r8[] = {8, 8, 8, 4};
   using P20 = SPlan<double, 20, 20, 20, 20, 5>;
-  run<P20, 100, 4>(2000, r20, -3, 1001 * 8, 1, reps);
-  using D16 = SPlan<double, 16, 16, 16, 16, 8>;
-  run<D16, 128, 2>(2048, r16, -3, 1025 * 8, 1, reps);
-  run<D16, 128, 3>(2048, r16, -3, 1025 * 8, 1, reps);
-  run<D16, 128, 4>(2048, r16, -3, 1025 * 8, 1, reps);
-  run<D16, 256, 2>(2048, r16, -3, 1025 * 8, 2, reps);
-  using D8 = SPlan<double, 8, 8, 8, 8, 8, 4>;
-  run<D8, 256, 2>(2048, r8, -4, 1025 * 8, 1, reps);
-  run<D8, 256, 3>(2048, r8, -4, 1025 * 8, 1, reps);
+  run<P20, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
   using F20 = SPlan<float, 20, 80, 20, 20, 5>;
-  run<F20, 100, 4>(2000, r20, -3, 1001 * 8, 1, reps);
-  using F16 = SPlan<float, 16, 16, 16, 16, 8>;
-  run<F16, 128, 2>(2048, r16, -3, 1025 * 8, 1, reps);
-  run<F16, 128, 4>(2048, r16, -3, 1025 * 8, 1, reps);
-  run<F16, 128, 6>(2048, r16, -3, 1025 * 8, 1, reps);
-  run<F16, 256, 2>(2048, r16, -3, 1025 * 8, 2, reps);
+  run<F20, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
   return 0;
 }
