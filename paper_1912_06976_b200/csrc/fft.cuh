@@ -323,13 +323,20 @@ __device__ __forceinline__ void spass_store(const cplx<T> (&v)[E], cplx<T>* sm, 
 
 // `active` = false: the thread follows the same control flow and barriers but
 // touches no shared memory (helper lanes that pad a team to whole warps).
-template <class T, int E, int L, int PAD, int NS, int R, int... Rest>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// hook() runs once, before the first exchange's barrier (e.g. to wait for an
+// asynchronous copy that still reads the exchange buffer)
+template <class T, int E, int L, int PAD, int NS, int R, int... Rest, class Hook = NoHook>
 __device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
-                                     bool active = true) {
+                                     bool active = true, Hook hook = Hook{}) {
   constexpr int NT = L / E;
   static_assert(E % R == 0, "radix must divide elements per thread");
   spass_compute<T, E, R, NS, NT, L>(v, active ? t : 0, tw);
   if constexpr (sizeof...(Rest) > 0) {
+    if constexpr (NS == 1) hook();
     __syncthreads();
     spass_store<T, E, R, NS, NT, PAD>(v, sm, t, active);
     __syncthreads();
@@ -359,6 +366,11 @@ struct SPlan {
   __device__ __forceinline__ static void fft_masked(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
                                                     bool active) {
     sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw, active);
+  }
+  template <class Hook>
+  __device__ __forceinline__ static void fft_hook(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
+                                                  Hook hook) {
+    sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw, true, hook);
   }
 };
 

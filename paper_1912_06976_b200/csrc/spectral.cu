@@ -25,6 +25,12 @@
 #include "spectral.h"
 #include "tma.cuh"
 
+#ifndef ROW_REGS_F32
+#define ROW_REGS_F32 128  // register target of the fp32 row passes (80, 96 measured slower)
+#endif
+#ifndef COL_REGS_F32
+#define COL_REGS_F32 168  // register target of the fp32 column stages (96, 128 measured slower)
+#endif
 #ifndef T2D_TEAMS
 #define T2D_TEAMS 1  // row pairs (teams) per CTA of the tensor-TMA row passes
 #endif
@@ -912,12 +918,16 @@ __global__ void __launch_bounds__(MAXT, MINB)
       const bool inb = i < a.nvalid;
       v[k] = mkc<V>(inb ? rows[i] : T(0), inb && vb ? rows[rowcap + i] : T(0));
     }
-    __syncthreads();  // rows consumed; also orders the previous tile's TMA store read (below)
+    __syncthreads();  // rows consumed
     if (t == 0 && item + (int)gridDim.x < total) {
       fence_proxy_async();
       issue(item + gridDim.x);
     }
-    PL::fft(v, sm, t, d);
+    // the previous tile's TMA store may still be reading sm: wait only right
+    // before the first exchange overwrites it (after the first radix pass)
+    PL::fft_hook(v, sm, t, d, [&] {
+      if (t == 0 && it > 0) tma_store_wait_read();
+    });
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
@@ -948,10 +958,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
       const int s = item / npairs, qa = 2 * (item - s * npairs);
       for (int kx0 = 0; kx0 < HX; kx0 += kBoxKx) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
       tma_store_commit();
-      tma_store_wait_read();  // the tile region is the next FFT's exchange buffer
     }
-    __syncthreads();
   }
+  if (t == 0) tma_store_wait_read();
 }
 
 template <class PL, int MAXT, int MINB, int TEAMS>
@@ -1053,6 +1062,11 @@ template <class P> struct Tag { using type = P; };
 
 // opt-in (BTTB_COL_E10=1): measured slower on C4 fp64 (9.2 vs 7.7 ms/step) --
 // the third shared-memory exchange costs more than the occupancy it buys
+bool row_e10() {
+  static const bool on = getenv("BTTB_ROW_E10") && atoi(getenv("BTTB_ROW_E10")) != 0;
+  return on;
+}
+
 bool col_e10() {
   static const bool on = getenv("BTTB_COL_E10") && atoi(getenv("BTTB_COL_E10")) != 0;
   return on;
@@ -1060,10 +1074,11 @@ bool col_e10() {
 
 // COL selects the plan of the accumulating column kernels where it differs
 // (fp64 L=2000: 10 elements per thread keeps the E-element accumulator cheap)
-template <class T, bool COL = false, class F>
+template <class T, bool COL = false, bool ROW = false, class F>
 cudaError_t with_plan(int L, int E, F&& f) {
   if constexpr (sizeof(T) == 8) {
     if (COL && L == 2000 && col_e10()) return f(Tag<SPlan<double, 10, 40, 10, 10, 10, 2>>{});
+    if (ROW && L == 2000 && row_e10()) return f(Tag<SPlan<double, 10, 40, 10, 10, 10, 2>>{});
     switch (L) {
       case 2048: return f(Tag<SPlan<double, 8, 8, 8, 8, 8, 4>>{});
       case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
@@ -1117,8 +1132,12 @@ template <class PL> struct Shape {
     return 2048 / (warps(threads) * regs) > 1 ? 2048 / (warps(threads) * regs) : 1;
   }
   // register targets: the column kernels keep E-element accumulators beside the data
-  static constexpr int col_regs = 64 + 4 * PL::E * (int)(sizeof(T) / 4) > 255 ? 255 : 64 + 4 * PL::E * (int)(sizeof(T) / 4);
-  static constexpr int col_regs_rounded = col_regs <= 128 ? 128 : (col_regs <= 144 ? 144 : (col_regs <= 168 ? 168 : 255));
+  static constexpr int col_regs = sizeof(T) == 4 ? COL_REGS_F32
+                                  : (64 + 4 * PL::E * 2 > 255 ? 255 : 64 + 4 * PL::E * 2);
+  static constexpr int col_regs_rounded =
+      col_regs <= 96 ? 96 : col_regs <= 128 ? 128 : (col_regs <= 144 ? 144 : (col_regs <= 168 ? 168 : 255));
+  // row passes hold E complex values plus the separated tile: fp32 needs far fewer registers
+  static constexpr int row_regs = sizeof(T) == 8 ? 128 : ROW_REGS_F32;
   static constexpr int row_minb = PL::kStatic ? minb(row_threads, 128) : 1;
   // fp64 plans with 20 elements per thread keep the column accumulator in
   // shared memory (registers would cap occupancy at two teams per SM)
@@ -1128,7 +1147,7 @@ template <class PL> struct Shape {
   static constexpr int tma_minb = PL::kStatic ? minb(col_threads, col_regs_rounded) : 1;
   static constexpr int rowtma_minb = PL::kStatic ? minb(NT, 128) : 1;
   static constexpr int t2d_teams = T2D_TEAMS;
-  static constexpr int t2d_minb = PL::kStatic ? minb(T2D_TEAMS * NT, 128) : 1;
+  static constexpr int t2d_minb = PL::kStatic ? minb(T2D_TEAMS * NT, row_regs) : 1;
 };
 
 bool tma_ok() {
@@ -1276,7 +1295,7 @@ int persistent_grid(K kern, int threads, size_t smem, int items) {
 template <class T>
 cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
-  return with_plan<T>(d.L, E, [&](auto tag) {
+  return with_plan<T, false, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
       const size_t esz = sizeof(T);
@@ -1331,7 +1350,7 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
 template <class T>
 cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st) {
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
-  return with_plan<T>(d.L, E, [&](auto tag) {
+  return with_plan<T, false, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
       const size_t esz = sizeof(cplx<T>);
