@@ -800,12 +800,13 @@ template <class V> __host__ __device__ __forceinline__ int stage_offset(int slot
 template <class PL> struct RowTile {
   static constexpr int HX = PL::L / 2 + 1;
   static constexpr int NI = (HX + PL::NT - 1) / PL::NT;  // kx items per thread
-  static constexpr int NBOX = (HX + kBoxKx - 1) / kBoxKx;
+  static constexpr int BOXK = HX < kBoxKx ? HX : kBoxKx;  // box extent along kx (the tensor map's)
+  static constexpr int NBOX = (HX + BOXK - 1) / BOXK;
   // shared slots (complex) of one team: exchange buffer or staged box, whichever
   // is larger, rounded to 128 bytes (tensor-TMA shared addresses are 128-B aligned)
   static constexpr int slots(int exchange_slots) {
     constexpr int per = 128 / (int)sizeof(cplx<typename PL::Scalar>);
-    const int n = exchange_slots > 2 * NBOX * kBoxKx ? exchange_slots : 2 * NBOX * kBoxKx;
+    const int n = exchange_slots > 2 * NBOX * BOXK ? exchange_slots : 2 * NBOX * BOXK;
     return (n + per - 1) / per * per;
   }
 };
@@ -863,7 +864,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   fence_proxy_async();
   __syncthreads();
   if (t == 0 && active) {
-    for (int kx0 = 0; kx0 < HX; kx0 += kBoxKx) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
+    for (int kx0 = 0; kx0 < HX; kx0 += RT::BOXK) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
     tma_store_commit();
     tma_store_wait_read();
   }
@@ -956,7 +957,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
     __syncthreads();
     if (t == 0) {
       const int s = item / npairs, qa = 2 * (item - s * npairs);
-      for (int kx0 = 0; kx0 < HX; kx0 += kBoxKx) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
+      for (int kx0 = 0; kx0 < HX; kx0 += RT::BOXK) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
       tma_store_commit();
     }
   }
@@ -980,8 +981,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
   if (t == 0 && active) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * kBoxKx * 2 * sizeof(V)));
-    for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * kBoxKx, &imap, 2 * ja, b * kBoxKx, s, bar);
+    // every box delivers its full extent (out-of-range rows zero-filled)
+    mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * RT::BOXK * 2 * sizeof(V)));
+    for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
   }
   __syncthreads();
   if (active) mbar_wait(bar, 0);
@@ -1297,7 +1299,7 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
   return with_plan<T, false, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+    if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(T);
       if (row_tma_ok() && al16(a.in) && (a.nvalid * esz) % 16 == 0 && (a.ld_in * esz) % 16 == 0 &&
           (a.in_sstride * esz) % 16 == 0 && (a.in_bstride * esz) % 16 == 0) {
@@ -1352,7 +1354,7 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nslabs <= 0 || a.nrows <= 0) return cudaSuccess;
   return with_plan<T, false, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+    if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(cplx<T>);
       const int rowcap = (a.Hx + 1) & ~1;
       if (row_tma_ok() && a.rowmajor && al16(a.in) && a.ld_in >= rowcap && (a.ld_in * esz) % 16 == 0 &&
@@ -1394,7 +1396,7 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
+    if constexpr (PL::kStatic && PL::NT >= 32 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
                   (PL::E * 4) % 16 == 0) {
       if (tma_ok() && tmem_ok() && (a.lds * 16) % 16 == 0 && (a.s_rstride * 16) % 16 == 0) {
         auto kern = k_col_fwd_tmem<PL, 3>;
@@ -1406,7 +1408,7 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
         return cudaGetLastError();
       }
     }
-    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+    if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
           (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
@@ -1436,7 +1438,7 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
+    if constexpr (PL::kStatic && PL::NT >= 32 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
                   (PL::E * 4) % 16 == 0) {
       if (tma_ok() && tmem_ok()) {
         auto kern = k_col_tra_tmem<PL, 3>;
@@ -1448,7 +1450,7 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
         return cudaGetLastError();
       }
     }
-    if constexpr (PL::kStatic && Shape<PL>::col_teams == 1) {
+    if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
         auto kern = k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
