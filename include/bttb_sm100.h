@@ -60,6 +60,14 @@ typedef struct bttb_plan_s bttb_plan;
 int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype, int device,
                      int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly);
 
+/* Replaces load_stack (transform.py:135-159): a plan whose spectrum cache is
+ * uploaded from host memory (local layers x Hx x Ly complex of the plan dtype,
+ * as bttb_layer_spectrum returns them) instead of being rebuilt.  Lx, Ly must
+ * be the lengths the spectra were built at. */
+int bttb_plan_create_from_spectra(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
+                                  int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
+                                  const void* host_spectra);
+
 int bttb_plan_destroy(bttb_plan* plan);
 
 /* Replaces apply(stack, x, mode) (multiply.py:22-58) for `batch` vectors.

@@ -624,8 +624,9 @@ const char* bttb_version(void) { return "bttb_sm100 0.1.0 (sm_100a)"; }
 
 int64_t bttb_fft_length(int64_t n) { return pick_length(n); }
 
-int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype, int device,
-                     int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly) {
+static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
+                            int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
+                            const void* host_spectra) {
   g_err.clear();
   if (!out || !grid || !kernel) return fail(BTTB_EINVAL, "null argument");
   *out = nullptr;
@@ -700,7 +701,15 @@ int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* 
            cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) rc = fail(BTTB_ECUDA, "cannot create the plan streams/events");
   }
-  if (!rc) rc = build_spectra(p);
+  if (!rc) {
+    if (host_spectra) {
+      const size_t bytes = (size_t)p->nzl * p->Hx * p->Ly * p->elem;
+      cudaError_t ce = cudaMemcpy(p->spectra, host_spectra, bytes, cudaMemcpyHostToDevice);
+      if (ce != cudaSuccess) rc = fail(BTTB_ECUDA, "spectrum upload: %s", cudaGetErrorString(ce));
+    } else {
+      rc = build_spectra(p);
+    }
+  }
   if (rc) {
     std::string msg = g_err;
     destroy_plan(p);
@@ -709,6 +718,19 @@ int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* 
   }
   *out = p;
   return BTTB_OK;
+}
+
+int bttb_plan_create(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype, int device,
+                     int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly) {
+  return plan_create_impl(out, grid, kernel, dtype, device, layer_begin, layer_end, Lx, Ly, nullptr);
+}
+
+int bttb_plan_create_from_spectra(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
+                                  int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
+                                  const void* host_spectra) {
+  if (!host_spectra) return fail(BTTB_EINVAL, "null spectra");
+  if (Lx <= 0 || Ly <= 0) return fail(BTTB_EINVAL, "FFT lengths must be given for cached spectra");
+  return plan_create_impl(out, grid, kernel, dtype, device, layer_begin, layer_end, Lx, Ly, host_spectra);
 }
 
 int bttb_plan_destroy(bttb_plan* plan) {

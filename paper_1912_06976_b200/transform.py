@@ -13,6 +13,7 @@ half spectrum per layer is generated and kept in HBM by the sm_100a library
   it is not stored;
 * the 1/(Lx*Ly) inverse normalisation is folded into the cached spectrum.
 """
+import struct
 import threading
 
 import numpy as np
@@ -21,7 +22,7 @@ from . import _lib
 from .grid import GridSpec
 
 __all__ = ["TransformStack", "build_transform_stack", "transpose_layout",
-           "circulant_extension_column", "fft_length"]
+           "circulant_extension_column", "fft_length", "save_stack", "load_stack"]
 
 _DTYPES = {"float64": _lib.F64, "float32": _lib.F32}
 
@@ -42,8 +43,9 @@ class TransformStack:
     :meth:`layer_spectrum`.
     """
 
-    def __init__(self, handle, grid, kind, dtype, device, layer_range, evals):
+    def __init__(self, handle, grid, kind, dtype, device, layer_range, evals, params=None):
         self._handle = handle
+        self.params = params
         self._lock = threading.Lock()
         self.grid = grid
         self.kind = kind
@@ -159,7 +161,94 @@ def build_transform_stack(grid, params, dtype="float64", device=0, layers=None, 
                                            _lib.ctypes.byref(k), _DTYPES[dtype], int(device),
                                            lo, hi, int(lx), int(ly)))
     return TransformStack(h, grid, params.kind, dtype, int(device), (lo, hi),
-                          _evals(grid, params.kind))
+                          _evals(grid, params.kind), params)
+
+
+# ---------------------------------------------------------------------------
+# persistence (transform.py:107-159 of the reference)
+# ---------------------------------------------------------------------------
+_MAGIC = b"BTB2"
+_VERSION = 1
+_KIND_CODES = {"gravity": 0, "magnetic": 1}
+_DTYPE_CODES = {"float64": 0, "float32": 1}
+
+
+def save_stack(stack, path):
+    """Persist a device stack: its half spectra as cached, plus what rebuilds the plan.
+
+    Little-endian layout: magic "BTB2" (not the reference's "BTTB": the payload
+    is the device cache, (Hx, Ly) half spectra at FFT lengths (Lx, Ly), scaled
+    by 1/(Lx*Ly), instead of two full complex128 (mx, my) stacks), version u32,
+    kind u8, dtype u8, grid counts 7 x i64, spacings 2 x f64, nz+1 depths,
+    gamma*scale f64, gc 5 x f64, kernel D, I, F 3 x f64, layer range 2 x i64,
+    Lx, Ly 2 x i64, then layer_end-layer_begin spectra.  Loading gives
+    bit-identical products (the spectra are not recomputed).
+    """
+    g = stack.grid
+    p = stack.params
+    if p is None:
+        raise ValueError("stack has no kernel parameters to persist")
+    lx, ly = stack.fft_shape
+    with open(path, "wb") as fh:
+        fh.write(_MAGIC)
+        fh.write(struct.pack("<IBB", _VERSION, _KIND_CODES[stack.kind], _DTYPE_CODES[str(stack.dtype)]))
+        fh.write(struct.pack("<7q", g.sx, g.sy, g.nz, g.pxl, g.pxr, g.pyl, g.pyr))
+        fh.write(struct.pack("<2d", g.dx, g.dy))
+        fh.write(np.asarray(g.z_blocks, dtype="<f8").tobytes())
+        gc = list(p.gc) if p.kind == "magnetic" else [0.0] * 5
+        fh.write(struct.pack("<6d", p.gamma * p.scale, *gc))
+        fh.write(struct.pack("<3d", p.D, p.I, p.F))
+        fh.write(struct.pack("<4q", stack.layer_begin, stack.layer_end, lx, ly))
+        for r in range(stack.nz_local):
+            fh.write(np.ascontiguousarray(stack.layer_spectrum(r)).tobytes())
+
+
+def load_stack(path, device=0):
+    """Read back a stack written by :func:`save_stack` onto a device (no rebuild)."""
+    from .grid import make_grid
+    from .kernels import GRAVITATIONAL_CONST, KernelParams
+
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic == b"BTTB":
+            raise ValueError("reference-format stack file (full complex128 spectra at the "
+                             "minimal embedding): rebuild it with build_transform_stack")
+        if magic != _MAGIC:
+            raise ValueError(f"not a transform-stack file (magic {magic!r})")
+        version, kind_code, dt_code = struct.unpack("<IBB", fh.read(6))
+        if version != _VERSION:
+            raise ValueError(f"unsupported stack version {version}")
+        sx, sy, nz, pxl, pxr, pyl, pyr = struct.unpack("<7q", fh.read(56))
+        dx, dy = struct.unpack("<2d", fh.read(16))
+        z = np.frombuffer(fh.read(8 * (nz + 1)), dtype="<f8")
+        gs, *gc = struct.unpack("<6d", fh.read(48))
+        D, I, F = struct.unpack("<3d", fh.read(24))  # noqa: E741
+        lo, hi, lx, ly = struct.unpack("<4q", fh.read(32))
+        grid = make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, z)
+        kind = {0: "gravity", 1: "magnetic"}[kind_code]
+        dtype = {0: "float64", 1: "float32"}[dt_code]
+        hx = lx // 2 + 1
+        cdt = np.dtype("<c16" if dtype == "float64" else "<c8")
+        count = (hi - lo) * hx * ly
+        buf = fh.read(count * cdt.itemsize)
+        if len(buf) != count * cdt.itemsize:
+            raise ValueError("truncated transform-stack file")
+    spectra = np.frombuffer(buf, dtype=cdt)
+    if kind == "gravity":
+        params = KernelParams(kind="gravity", gamma=GRAVITATIONAL_CONST, scale=gs / GRAVITATIONAL_CONST)
+    else:
+        params = KernelParams(kind="magnetic", D=D, I=I, F=F, gc=tuple(gc))
+    zc = np.ascontiguousarray(grid.z_blocks, dtype=float)
+    g = _lib.BttbGrid(grid.sx, grid.sy, grid.nz, grid.pxl, grid.pxr, grid.pyl, grid.pyr,
+                      grid.dx, grid.dy, _lib.as_dptr(zc))
+    k = params.native()
+    if kind == "gravity":
+        k.gamma_scaled = gs  # exactly the persisted multiplier
+    h = _lib.ctypes.c_void_p()
+    _lib.check(_lib.lib().bttb_plan_create_from_spectra(
+        _lib.ctypes.byref(h), _lib.ctypes.byref(g), _lib.ctypes.byref(k), _DTYPES[dtype], int(device),
+        lo, hi, lx, ly, spectra.ctypes.data_as(_lib.ctypes.c_void_p)))
+    return TransformStack(h, grid, kind, dtype, int(device), (lo, hi), 0, params)
 
 
 def transpose_layout(T):
