@@ -1239,10 +1239,19 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// TMEM-resident column accumulators: opt-in (BTTB_TMEM=1); correct, but
-// measured slower on C4 fp64 (7.72 vs 7.21 ms/step)
-bool tmem_ok() {
-  static const bool on = getenv("BTTB_TMEM") && atoi(getenv("BTTB_TMEM")) != 0;
+// TMEM-resident column state.  Transpose (data spectrum in TMEM): default on,
+// measured 2.84 vs 2.95 ms per C4 fp64 transpose; forward (accumulator in
+// TMEM): opt-in, measured 2.98 vs 2.60 ms.  BTTB_TMEM=0/1 overrides both.
+bool env_flag(const char* name, bool dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) != 0 : dflt;
+}
+bool tmem_fwd_ok() {
+  static const bool on = env_flag("BTTB_TMEM_FWD", env_flag("BTTB_TMEM", false));
+  return on;
+}
+bool tmem_tra_ok() {
+  static const bool on = env_flag("BTTB_TMEM_TRA", env_flag("BTTB_TMEM", true));
   return on;
 }
 
@@ -1398,7 +1407,7 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && PL::NT >= 32 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
                   (PL::E * 4) % 16 == 0) {
-      if (tma_ok() && tmem_ok() && (a.lds * 16) % 16 == 0 && (a.s_rstride * 16) % 16 == 0) {
+      if (tma_ok() && tmem_fwd_ok()) {
         auto kern = k_col_fwd_tmem<PL, 3>;
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * 16 + 16;
         cudaError_t e = set_smem(kern, smem);
@@ -1440,7 +1449,7 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && PL::NT >= 32 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
                   (PL::E * 4) % 16 == 0) {
-      if (tma_ok() && tmem_ok()) {
+      if (tma_ok() && tmem_tra_ok()) {
         auto kern = k_col_tra_tmem<PL, 3>;
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * 16 + 16;
         cudaError_t e = set_smem(kern, smem);
