@@ -17,6 +17,7 @@
 // they stay L2-resident between the row and column kernels.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -295,9 +296,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   uint64_t* bars = reinterpret_cast<uint64_t*>(ybuf + ((nv + 1) & ~1));
   const int t = threadIdx.x;
   const int kx = blockIdx.x, b = blockIdx.y;
+  // layer split (gridDim.z > 1): this CTA sums layers [r0, r1) and adds its
+  // part of W atomically (two splits onto a zeroed W: exact and order-free)
+  const int r0 = (a.K * (int)blockIdx.z) / (int)gridDim.z, K = (a.K * ((int)blockIdx.z + 1)) / (int)gridDim.z - r0;
   const uint32_t ybytes = nv * sizeof(V), sbytes = L * sizeof(V);
-  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
-  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy + (long long)r0 * a.y_rstride;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds + (long long)r0 * a.s_rstride;
   const uint64_t pol = policy_evict_first();
   if (t == 0) {
     mbar_init(&bars[0], 1);
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   V acc[E], v[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
-  for (int r = 0; r < a.K; ++r) {
+  for (int r = 0; r < K; ++r) {
     mbar_wait(&bars[0], r & 1);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
       v[k] = q < nv ? ybuf[q] : mkc<V>(T(0), T(0));
     }
     __syncthreads();
-    if (t == 0 && r + 1 < a.K) {
+    if (t == 0 && r + 1 < K) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], ybytes);
       tma_load(ybuf, Yb + (long long)(r + 1) * a.y_rstride, ybytes, &bars[0], pol);
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
       acc[k].y += w.x * v[k].y + w.y * v[k].x;
     }
     __syncthreads();
-    if (t == 0 && r + 1 < a.K) {
+    if (t == 0 && r + 1 < K) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[1], sbytes);
       tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[1], pol);
@@ -349,8 +353,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
     const int j = t + NT * k;
     if (j < a.nout) {
       V val = conjv(acc[k]);
-      if (a.accumulate) val = val + wc[j];
-      wc[j] = val;
+      if (gridDim.z > 1) {
+        atomicAdd(&wc[j].x, val.x);
+        atomicAdd(&wc[j].y, val.y);
+      } else {
+        if (a.accumulate) val = val + wc[j];
+        wc[j] = val;
+      }
     }
   }
 }
@@ -367,8 +376,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
   uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + L);
   const int t = threadIdx.x;
   const int kx = blockIdx.x, b = blockIdx.y;
+  const int r0 = (a.K * (int)blockIdx.z) / (int)gridDim.z, K = (a.K * ((int)blockIdx.z + 1)) / (int)gridDim.z - r0;
   const uint32_t sbytes = L * sizeof(V);
-  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds + (long long)r0 * a.s_rstride;
   const uint64_t pol = policy_evict_first();
   if (t == 0) {
     mbar_init(&bars[0], 1);
@@ -385,9 +395,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
   }
   __syncthreads();
   PL::fft(dh, sm, t, d);
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw);
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw) +
+          (long long)r0 * a.w_rstride;
   const long long qstride = a.rowmajor ? a.ldw : 1;
-  for (int r = 0; r < a.K; ++r) {
+  for (int r = 0; r < K; ++r) {
     mbar_wait(&bars[0], r & 1);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -396,7 +407,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
       v[k] = mkc<V>(w.x * dh[k].x + w.y * dh[k].y, w.y * dh[k].x - w.x * dh[k].y);
     }
     __syncthreads();
-    if (t == 0 && r + 1 < a.K) {
+    if (t == 0 && r + 1 < K) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], sbytes);
       tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[0], pol);
@@ -551,8 +562,9 @@ __global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_tra_tmem(ColTraA
   const int t = threadIdx.x, warp = t / 32;
   const bool active = t < NT;
   const int kx = blockIdx.x, b = blockIdx.y;
+  const int r0 = (a.K * (int)blockIdx.z) / (int)gridDim.z, K = (a.K * ((int)blockIdx.z + 1)) / (int)gridDim.z - r0;
   const uint32_t sbytes = L * sizeof(V);
-  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds + (long long)r0 * a.s_rstride;
   const uint64_t pol = policy_evict_first();
   if (warp == 0) tmem_alloc<TC::NCOLS>(taddr_s);
   if (t == 0) {
@@ -581,9 +593,10 @@ __global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_tra_tmem(ColTraA
     tmem_st16(ta + 16 * g, u);
   }
   tmem_wait_st();
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw);
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw) +
+          (long long)r0 * a.w_rstride;
   const long long qstride = a.rowmajor ? a.ldw : 1;
-  for (int r = 0; r < a.K; ++r) {
+  for (int r = 0; r < K; ++r) {
     mbar_wait(bar, r & 1);
 #pragma unroll
     for (int g = 0; g < TC::GROUPS; ++g) {
@@ -600,7 +613,7 @@ __global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_tra_tmem(ColTraA
       }
     }
     __syncthreads();
-    if (t == 0 && r + 1 < a.K) {
+    if (t == 0 && r + 1 < K) {
       fence_proxy_async();
       mbar_arrive_expect_tx(bar, sbytes);
       tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, bar, pol);
@@ -1294,6 +1307,20 @@ int sm_count() {
   return n;
 }
 
+// Layer splits of the transpose column stage: each column CTA runs all its
+// layers, so Hx CTAs on ~300-450 resident CTAs leave the last wave partly idle;
+// splitting a column's layers into s parts (each redoes the cheap data-column
+// FFT) multiplies the CTA count.  Output values do not depend on s.  Measured
+// on C4 fp64: 2.90 -> 2.79 ms per transpose.  (The forward does not split: its
+// halves would have to be summed, and a split measured no faster.)
+int layer_splits(long ctas, int layers) {
+  static const char* env = getenv("BTTB_LAYER_SPLITS");
+  if (env) return atoi(env) > 0 ? atoi(env) : 1;
+  int sp = 1;
+  while (sp < 4 && ctas * sp < 2000 && layers >= 16 * 2 * sp) sp *= 2;
+  return sp;
+}
+
 // grid of a persistent kernel: every SM filled to its occupancy, never more CTAs than items
 template <class K>
 int persistent_grid(K kern, int threads, size_t smem, int items) {
@@ -1425,7 +1452,14 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
+        // two layer halves would add into a zeroed W (exact, order-free); opt-in only
+        const char* fs = getenv("BTTB_FWD_SPLITS");
+        const int sp = (a.accumulate || !fs) ? 1 : (atoi(fs) == 2 ? 2 : 1);
+        if (sp > 1) {
+          e = cudaMemsetAsync(a.W, 0, (size_t)a.nbatch * a.w_bstride * esz, st);
+          if (e != cudaSuccess) return e;
+        }
+        dim3 grd(a.Hx, a.nbatch, sp), blk(PL::NT);
         kern<<<grd, blk, smem, st>>>(a, d);
         return cudaGetLastError();
       }
@@ -1454,7 +1488,8 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * 16 + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        dim3 grd(a.Hx, a.nbatch), blk(TmemCfg<PL>::NTR);
+        const int sp = layer_splits((long)a.Hx * a.nbatch, a.K);
+        dim3 grd(a.Hx, a.nbatch, sp), blk(TmemCfg<PL>::NTR);
         kern<<<grd, blk, smem, st>>>(a, d);
         return cudaGetLastError();
       }
@@ -1466,7 +1501,8 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
-        dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
+        const int sp = layer_splits((long)a.Hx * a.nbatch, a.K);
+        dim3 grd(a.Hx, a.nbatch, sp), blk(PL::NT);
         kern<<<grd, blk, smem, st>>>(a, d);
         return cudaGetLastError();
       }
