@@ -104,11 +104,36 @@ struct RadixPlan {
   }
 };
 
+// Per-pass twiddle tables of a radix sequence: for each pass p with NS > 1,
+// entry (r-1)*NS + k = exp(-2*pi*i*r*k/(NS*R)), r < R, k < NS (fft.cuh sfft).
+template <class C>
+std::vector<C> per_pass_table(const int* radix, int npass) {
+  std::vector<C> out;
+  long ns = 1;
+  for (int p = 0; p < npass; ++p) {
+    const int R = radix[p];
+    if (ns > 1)
+      for (int r = 1; r < R; ++r)
+        for (long k = 0; k < ns; ++k) {
+          const long double ang = 2.0L * 3.141592653589793238462643383279502884L * (long double)(r * k) /
+                                  (long double)(ns * R);
+          C c;
+          c.x = (decltype(c.x))cosl(ang);
+          c.y = (decltype(c.y))(-sinl(ang));
+          out.push_back(c);
+        }
+    ns *= R;
+  }
+  return out;
+}
+
 struct FFTPlanHost {
   int L = 0;
   RadixPlan p64, p32;
   double2* tw64 = nullptr;
   float2* tw32 = nullptr;
+  double2* twp64 = nullptr;  // per-pass tables of the registered compile-time plans (or null)
+  float2* twp32 = nullptr;
 
   int init(int64_t len) {
     L = (int)len;
@@ -129,13 +154,30 @@ struct FFTPlanHost {
     CU(cudaMalloc(&tw32, sizeof(float2) * L));
     CU(cudaMemcpy(tw64, h64.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(tw32, h32.data(), sizeof(float2) * L, cudaMemcpyHostToDevice));
+    int rad[16];
+    int np = static_radices(L, true, rad);
+    if (np > 0) {
+      std::vector<double2> t = per_pass_table<double2>(rad, np);
+      CU(cudaMalloc(&twp64, sizeof(double2) * std::max<size_t>(t.size(), 1)));
+      if (!t.empty()) CU(cudaMemcpy(twp64, t.data(), sizeof(double2) * t.size(), cudaMemcpyHostToDevice));
+    }
+    np = static_radices(L, false, rad);
+    if (np > 0) {
+      std::vector<float2> t = per_pass_table<float2>(rad, np);
+      CU(cudaMalloc(&twp32, sizeof(float2) * std::max<size_t>(t.size(), 1)));
+      if (!t.empty()) CU(cudaMemcpy(twp32, t.data(), sizeof(float2) * t.size(), cudaMemcpyHostToDevice));
+    }
     return BTTB_OK;
   }
   void release() {
     if (tw64) cudaFree(tw64);
     if (tw32) cudaFree(tw32);
+    if (twp64) cudaFree(twp64);
+    if (twp32) cudaFree(twp32);
     tw64 = nullptr;
     tw32 = nullptr;
+    twp64 = nullptr;
+    twp32 = nullptr;
   }
   template <class T> const RadixPlan& plan() const {
     if constexpr (std::is_same<T, double>::value) return p64; else return p32;
@@ -143,7 +185,13 @@ struct FFTPlanHost {
   template <class T> int E() const { return plan<T>().E; }
   template <class T> FFTDesc<T> desc() const {
     FFTDesc<T> d;
-    if constexpr (std::is_same<T, double>::value) d.tw = tw64; else d.tw = tw32;
+    if constexpr (std::is_same<T, double>::value) {
+      d.tw = tw64;
+      d.twp = twp64;
+    } else {
+      d.tw = tw32;
+      d.twp = twp32;
+    }
     const RadixPlan& rp = plan<T>();
     d.L = L;
     d.nt = rp.nt;

@@ -164,7 +164,8 @@ template <int PAD> __host__ __device__ __forceinline__ int pad_slot(int i) { ret
 // Plan for one transform length, passed by value to kernels.
 template <class T>
 struct FFTDesc {
-  const cplx<T>* tw;  // tw[m] = exp(-2*pi*i*m/L), m < L
+  const cplx<T>* tw;   // tw[m] = exp(-2*pi*i*m/L), m < L
+  const cplx<T>* twp;  // per-pass tables of this length's compile-time plan (see sfft), or null
   int L;              // transform length
   int nt;             // threads per team = L / E
   int npass;
@@ -285,7 +286,10 @@ __device__ __forceinline__ void team_fft(cplx<T> (&v)[E], cplx<T>* sm, int t, co
 // twiddle stride and the team size are constants, so the index arithmetic
 // folds (no runtime integer division) and every pass is fully unrolled.
 // ---------------------------------------------------------------------------
-template <class T, int E, int R, int NS, int NT, int L>
+// PP (per-pass twiddles): tw points at this pass's table, entry (r-1)*NS + k =
+// exp(-2*pi*i*r*k/(NS*R)) -- a warp's loads for one r are then contiguous in k
+// instead of striding r*k*L/(NS*R) through the length-L table.
+template <class T, int E, int R, int NS, int NT, int L, bool PP = false>
 __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw) {
   using V = cplx<T>;
   constexpr int NB = E / R;
@@ -298,7 +302,10 @@ __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx
       const int k = (t + NT * b) % NS;
       sfor<1, R>([&](auto rc) {
         constexpr int r = decltype(rc)::value;
-        u[r] = cmul(u[r], __ldg(&tw[r * STRIDE * k]));
+        if constexpr (PP)
+          u[r] = cmul(u[r], __ldg(&tw[(r - 1) * NS + k]));
+        else
+          u[r] = cmul(u[r], __ldg(&tw[r * STRIDE * k]));
       });
     }
     dft<R>(u);
@@ -329,12 +336,14 @@ struct NoHook {
 
 // hook() runs once, before the first exchange's barrier (e.g. to wait for an
 // asynchronous copy that still reads the exchange buffer)
-template <class T, int E, int L, int PAD, int NS, int R, int... Rest, class Hook = NoHook>
+// PP: tw is the per-pass table block (OFF = this pass's offset in it);
+// otherwise tw is the length-L table.
+template <class T, int E, int L, int PAD, bool PP, int OFF, int NS, int R, int... Rest, class Hook = NoHook>
 __device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
                                      bool active = true, Hook hook = Hook{}) {
   constexpr int NT = L / E;
   static_assert(E % R == 0, "radix must divide elements per thread");
-  spass_compute<T, E, R, NS, NT, L>(v, active ? t : 0, tw);
+  spass_compute<T, E, R, NS, NT, L, PP>(v, active ? t : 0, PP ? tw + OFF : tw);
   if constexpr (sizeof...(Rest) > 0) {
     if constexpr (NS == 1) hook();
     __syncthreads();
@@ -343,15 +352,26 @@ __device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const 
 #pragma unroll
     for (int s = 0; s < E; ++s)
       if (active) v[s] = sm[pad_slot<PAD>(t + NT * s)];
-    sfft<T, E, L, PAD, NS * R, Rest...>(v, sm, t, tw, active);
+    sfft<T, E, L, PAD, PP, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R, Rest...>(v, sm, t, tw, active);
   }
 }
 
 // Plan concepts used by the kernels: Scalar, E, nt(d), slot(e), slots(L),
 // fft(v, sm, t, d); kStatic / NT for launch bounds.
-template <class T, int E_, int PAD, int... Rs>
-struct SPlan {
+// Total entries of the per-pass twiddle tables of a radix sequence.
+template <int NS, int... Rs> struct PassTw;
+template <int NS> struct PassTw<NS> { static constexpr int size = 0; };
+template <int NS, int R, int... Rest> struct PassTw<NS, R, Rest...> {
+  static constexpr int size = (NS > 1 ? (R - 1) * NS : 0) + PassTw<NS * R, Rest...>::size;
+};
+
+// PP = true: twiddles from d.twp, the per-pass tables the host builds for the
+// registered plan of this length (spectral.cu static_radices); PP = false:
+// the generic length-L table (plans that are not the registered one).
+template <class T, int E_, int PAD, bool PP, int... Rs>
+struct SPlanT {
   using Scalar = T;
+  static constexpr bool kPerPass = PP;
   static constexpr bool kStatic = true;
   static constexpr int E = E_;
   static constexpr int L = (Rs * ...);
@@ -360,19 +380,30 @@ struct SPlan {
   __host__ __device__ __forceinline__ static int nt(const FFTDesc<T>&) { return NT; }
   __host__ __device__ __forceinline__ static int slot(int e) { return pad_slot<PAD>(e); }
   __host__ __device__ __forceinline__ static int slots(int len) { return pad_slot<PAD>(len) + 1; }
+  __device__ __forceinline__ static const cplx<T>* table(const FFTDesc<T>& d) { return PP ? d.twp : d.tw; }
   __device__ __forceinline__ static void fft(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d) {
-    sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw);
+    sfft<T, E_, L, PAD, PP, 0, 1, Rs...>(v, sm, t, table(d));
   }
   __device__ __forceinline__ static void fft_masked(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
                                                     bool active) {
-    sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw, active);
+    sfft<T, E_, L, PAD, PP, 0, 1, Rs...>(v, sm, t, table(d), active);
   }
   template <class Hook>
   __device__ __forceinline__ static void fft_hook(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
                                                   Hook hook) {
-    sfft<T, E_, L, PAD, 1, Rs...>(v, sm, t, d.tw, true, hook);
+    sfft<T, E_, L, PAD, PP, 0, 1, Rs...>(v, sm, t, table(d), true, hook);
   }
 };
+
+template <class T, int E_, int PAD, bool PP, int... Rs>
+__host__ __device__ inline int radix_list(SPlanT<T, E_, PAD, PP, Rs...>, int* out) {
+  int n = 0;
+  ((out[n++] = Rs), ...);
+  return n;
+}
+
+template <class T, int E_, int PAD, int... Rs> using SPlan = SPlanT<T, E_, PAD, true, Rs...>;
+template <class T, int E_, int PAD, int... Rs> using SPlanG = SPlanT<T, E_, PAD, false, Rs...>;
 
 // Runtime-radix plan; MAXT bounds the CTA size (256 keeps registers free for
 // the common small lengths, 1024 is for teams of more than 256 threads).

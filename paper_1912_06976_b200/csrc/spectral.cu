@@ -1092,8 +1092,8 @@ bool col_e10() {
 template <class T, bool COL = false, bool ROW = false, class F>
 cudaError_t with_plan(int L, int E, F&& f) {
   if constexpr (sizeof(T) == 8) {
-    if (COL && L == 2000 && col_e10()) return f(Tag<SPlan<double, 10, 40, 10, 10, 10, 2>>{});
-    if (ROW && L == 2000 && row_e10()) return f(Tag<SPlan<double, 10, 40, 10, 10, 10, 2>>{});
+    if (COL && L == 2000 && col_e10()) return f(Tag<SPlanG<double, 10, 40, 10, 10, 10, 2>>{});
+    if (ROW && L == 2000 && row_e10()) return f(Tag<SPlanG<double, 10, 40, 10, 10, 10, 2>>{});
     switch (L) {
       case 2048: return f(Tag<SPlan<double, 8, 8, 8, 8, 8, 4>>{});
       case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
@@ -1130,6 +1130,21 @@ cudaError_t with_plan(int L, int E, F&& f) {
       default: return cudaErrorInvalidValue;
     }
   }
+}
+
+// Radix sequence of the registered compile-time plan of (L, dtype), for the
+// host to build that plan's per-pass twiddle tables; 0 if none.
+int static_radices(int L, bool fp64, int* out) {
+  int n = 0;
+  auto take = [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    if constexpr (PL::kStatic) {
+      n = radix_list(PL{}, out);
+    }
+    return cudaSuccess;
+  };
+  if (fp64) with_plan<double>(L, 0, take); else with_plan<float>(L, 0, take);
+  return n;
 }
 
 // Fixed launch shapes of the compile-time plans: teams per CTA and the

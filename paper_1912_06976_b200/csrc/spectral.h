@@ -80,7 +80,7 @@ template <class T> cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc
 template <class T> cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cudaStream_t st);
 template <class TS> cudaError_t launch_col_spec(const ColSpecArgs& a, const FFTDesc<double>& d, int E, cudaStream_t st);
 
-// kernels launched per call of each launcher (for the bench's launch count)
-int row_launches();
+// radix sequence of the registered compile-time plan of (L, dtype), 0 if none
+int static_radices(int L, bool fp64, int* out);
 
 }  // namespace bttb

@@ -111,9 +111,9 @@ void run(int L, const int* radices, int npass, int ncols, int C, int reps) {
 int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 20;
   const int r20[] = {20, 20, 5};
-  using P20 = SPlan<double, 20, 20, 20, 20, 5>;
+  using P20 = SPlanG<double, 20, 20, 20, 20, 5>;
   run<P20, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
-  using F20 = SPlan<float, 20, 80, 20, 20, 5>;
+  using F20 = SPlanG<float, 20, 80, 20, 20, 5>;
   run<F20, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
   return 0;
 }
