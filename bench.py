@@ -5,7 +5,7 @@
 
 One step = one forward G*m and one transpose G^T*d over the configured
 workload (BASELINE.json config C4 by default: magnetic, 1000x1000 stations,
-128 layers, 2000x2000 embedding).  Under torchrun every rank holds a
+128 layers, 1999x1999 embedding at 2048x2048 FFT lengths).  Under torchrun every rank holds a
 contiguous block of depth layers (strong scaling: the workload is fixed); the
 forward partial station vectors are summed with one NCCL all-reduce and the
 data vector is broadcast for the transpose (paper_1912_06976_b200/parallel.py).

@@ -68,6 +68,16 @@ int bttb_plan_create_from_spectra(bttb_plan** out, const bttb_grid* grid, const 
                                   int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
                                   const void* host_spectra);
 
+/* Replaces load_stack of a REFERENCE-format file (transform.py:130-159): a
+ * plan whose spectra are built on the GPU (embedding at (Lx, Ly), FFTs) from
+ * caller-supplied response windows -- local layers x mx x my float64,
+ * row-major, in the layer_response_window layout (kernels.py:158-184) -- as
+ * recovered from the file's fft2(T^circ) arrays.  Lx, Ly = 0 picks them.
+ * Returns BTTB_ENONFINITE if a window holds a non-finite value. */
+int bttb_plan_create_from_windows(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
+                                  int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
+                                  const double* host_windows);
+
 int bttb_plan_destroy(bttb_plan* plan);
 
 /* Replaces apply(stack, x, mode) (multiply.py:22-58) for `batch` vectors.
@@ -101,8 +111,10 @@ int bttb_gravity_response(const double* x, int64_t ncx, const double* y, int64_t
 int bttb_magnetic_response(const double* x, int64_t ncx, const double* y, int64_t ncy, const double* r2,
                            double z1, double z2, const double* gc, double* out, int device);
 
-/* Smallest supported FFT length >= n (2^a, a>=3; 2^a*3^b or 2^a*5^b with
- * a>=2, b>=1; at most 8192), or -1. */
+/* FFT length the plan picks for an embedding of n (at most 8192, or -1):
+ * the smallest supported length >= n (2^a, a>=3; 2^a*3^b or 2^a*5^b with
+ * a>=2, b>=1), except that a power of two within 5% of it is preferred when
+ * the library has a compile-time FFT plan for it (e.g. 1999 -> 2048). */
 int64_t bttb_fft_length(int64_t n);
 
 /* Last error message on the calling thread ("" if none). */

@@ -58,19 +58,23 @@ int length_family(int64_t L) {  // returns E (elements per thread) or 0
   return 0;
 }
 
-// Smallest supported length >= n.  BTTB_FFT_POW2=1 prefers a power of two
-// within 5% of it: tools/fftbench.cu measures 2048 at 1.16x (fp64) / 1.8x
-// (fp32) the per-point FFT rate of 2000, but the fused C4 operator measured
-// slower at 2048 (fp64 11.4 vs 8.5 ms/step), so it is off by default.
+// FFT length for an embedding of n: the smallest supported length >= n,
+// except that a power of two within 5% of it is preferred when it has a
+// compile-time plan (fp64 2048 with 16 elements per thread runs the team FFT
+// at 338 vs 246 Gpt/s for 2000; the C4 step measured 4.14 vs 5.00 ms).
+// BTTB_FFT_POW2=0 turns the preference off.
 int64_t pick_length(int64_t n) {
   int64_t best = -1;
   for (int64_t L = std::max<int64_t>(n, 8); L <= 8192; ++L)
     if (length_family(L)) { best = L; break; }
   if (best < 0) return -1;
-  static const bool pow2 = getenv("BTTB_FFT_POW2") && atoi(getenv("BTTB_FFT_POW2")) != 0;
+  static const bool pow2 = !(getenv("BTTB_FFT_POW2") && atoi(getenv("BTTB_FFT_POW2")) == 0);
   int64_t p2 = 8;
   while (p2 < n) p2 *= 2;
-  if (pow2 && p2 <= 8192 && p2 * 100 <= best * 105) return p2;
+  if (pow2 && p2 != best && p2 <= 8192 && p2 * 100 <= best * 105) {
+    int rad[16];
+    if (static_radices((int)p2, true, rad) > 0 && static_radices((int)p2, false, rad) > 0) return p2;
+  }
   return best;
 }
 
@@ -377,12 +381,21 @@ int layer_corners(bttb_plan_s* p, EntryScratch& s, int64_t layer, cudaStream_t s
   return BTTB_OK;
 }
 
-int build_spectra(bttb_plan_s* p) {
+// host_windows (optional): local layers x mx x my caller-supplied response
+// windows (the reference-format stack loader); otherwise entries are generated.
+int build_spectra(bttb_plan_s* p, const double* host_windows = nullptr) {
   std::vector<double> hx, hy;
-  corner_vectors(p, hx, hy);
   EntryScratch s;
-  int rc = s.init(hx, hy, p->kind);
-  DevBuf emb, yb;
+  DevBuf emb, yb, win;
+  int rc = BTTB_OK;
+  if (host_windows) {
+    rc = s.flag.ensure(sizeof(int));
+    if (!rc) rc = win.ensure(sizeof(double) * p->mx * p->my);
+    if (!rc && cudaMemset(s.flag.p, 0, sizeof(int)) != cudaSuccess) rc = fail(BTTB_ECUDA, "flag reset failed");
+  } else {
+    corner_vectors(p, hx, hy);
+    rc = s.init(hx, hy, p->kind);
+  }
   if (!rc) rc = emb.ensure(sizeof(double) * p->Lx * p->Ly);
   if (!rc) rc = yb.ensure(sizeof(double2) * p->Hx * p->Ly);
   if (rc) {
@@ -395,10 +408,18 @@ int build_spectra(bttb_plan_s* p) {
   const double scale = 1.0 / ((double)p->Lx * (double)p->Ly);
   for (int64_t r = 0; r < p->nzl && !rc; ++r) {
     const int64_t g = p->l0 + r;
-    rc = layer_corners(p, s, g, st);
-    if (rc) break;
-    cudaError_t e = launch_embed(ea, (const double*)s.cm.p, s.mc, (const double*)s.cx.p, (const double*)s.cy.p,
-                                 s.ncy, p->z[g], p->z[g + 1], gc5(p), (int*)s.flag.p, (double*)emb.p, st);
+    cudaError_t e;
+    if (host_windows) {
+      const size_t wn = (size_t)p->mx * p->my;
+      e = cudaMemcpyAsync(win.p, host_windows + (size_t)r * wn, sizeof(double) * wn, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = launch_embed_window(ea, (int)p->my, (const double*)win.p, (int*)s.flag.p,
+                                                    (double*)emb.p, st);
+    } else {
+      rc = layer_corners(p, s, g, st);
+      if (rc) break;
+      e = launch_embed(ea, (const double*)s.cm.p, s.mc, (const double*)s.cx.p, (const double*)s.cy.p, s.ncy,
+                       p->z[g], p->z[g + 1], gc5(p), (int*)s.flag.p, (double*)emb.p, st);
+    }
     if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "embed: %s", cudaGetErrorString(e)); break; }
     RowR2CArgs ra{};
     ra.in = emb.p;
@@ -434,6 +455,7 @@ int build_spectra(bttb_plan_s* p) {
   s.release();
   emb.release();
   yb.release();
+  win.release();
   return rc;
 }
 
@@ -680,7 +702,7 @@ int64_t bttb_fft_length(int64_t n) { return pick_length(n); }
 
 static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
                             int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
-                            const void* host_spectra) {
+                            const void* host_spectra, const double* host_windows = nullptr) {
   g_err.clear();
   if (!out || !grid || !kernel) return fail(BTTB_EINVAL, "null argument");
   *out = nullptr;
@@ -761,7 +783,7 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
       cudaError_t ce = cudaMemcpy(p->spectra, host_spectra, bytes, cudaMemcpyHostToDevice);
       if (ce != cudaSuccess) rc = fail(BTTB_ECUDA, "spectrum upload: %s", cudaGetErrorString(ce));
     } else {
-      rc = build_spectra(p);
+      rc = build_spectra(p, host_windows);
     }
   }
   if (rc) {
@@ -785,6 +807,13 @@ int bttb_plan_create_from_spectra(bttb_plan** out, const bttb_grid* grid, const 
   if (!host_spectra) return fail(BTTB_EINVAL, "null spectra");
   if (Lx <= 0 || Ly <= 0) return fail(BTTB_EINVAL, "FFT lengths must be given for cached spectra");
   return plan_create_impl(out, grid, kernel, dtype, device, layer_begin, layer_end, Lx, Ly, host_spectra);
+}
+
+int bttb_plan_create_from_windows(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
+                                  int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
+                                  const double* host_windows) {
+  if (!host_windows) return fail(BTTB_EINVAL, "null windows");
+  return plan_create_impl(out, grid, kernel, dtype, device, layer_begin, layer_end, Lx, Ly, nullptr, host_windows);
 }
 
 int bttb_plan_destroy(bttb_plan* plan) {

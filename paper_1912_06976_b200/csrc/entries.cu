@@ -186,6 +186,31 @@ cudaError_t launch_embed(const EmbedArgs& a, const double* cm, MagCorners mc, co
   return cudaGetLastError();
 }
 
+// circulant embedding of a caller-supplied window (mx x my, row-major) at
+// (Lx, Ly): the persisted-stack path (transform.py:85-88 applied to a window
+// recovered from a reference stack file)
+__global__ void k_embed_window(EmbedArgs a, int my, const double* __restrict__ win, int* flag,
+                               double* __restrict__ out) {
+  const int tx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ty = blockIdx.y;
+  if (tx >= a.Lx) return;
+  const int wa = emb_to_win(tx, a.sx, a.nx, a.Lx);
+  const int wb = emb_to_win(ty, a.sy, a.ny, a.Ly);
+  double v = 0.0;
+  if (wa >= 0 && wb >= 0) {
+    v = win[(long long)wa * my + wb];
+    flag_nonfinite(v, flag);
+  }
+  out[(long long)ty * a.Lx + tx] = v;
+}
+
+cudaError_t launch_embed_window(const EmbedArgs& a, int my, const double* win, int* flag, double* out,
+                                cudaStream_t st) {
+  dim3 blk(128), grd((a.Lx + 127) / 128, a.Ly);
+  k_embed_window<<<grd, blk, 0, st>>>(a, my, win, flag, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_window(const EmbedArgs& a, int mx, int my, const double* cm, MagCorners mc, const double* cx,
                           const double* cy, int ncy, double z1, double z2, GC5 gc, int* flag, double* out,
                           cudaStream_t st) {

@@ -28,6 +28,8 @@ cudaError_t launch_corners(int kind, const double* cx, int ncx, const double* cy
                            cudaStream_t st);
 cudaError_t launch_embed(const EmbedArgs& a, const double* cm, MagCorners mc, const double* cx, const double* cy,
                          int ncy, double z1, double z2, GC5 gc, int* flag, double* out, cudaStream_t st);
+cudaError_t launch_embed_window(const EmbedArgs& a, int my, const double* win, int* flag, double* out,
+                                cudaStream_t st);
 cudaError_t launch_window(const EmbedArgs& a, int mx, int my, const double* cm, MagCorners mc, const double* cx,
                           const double* cy, int ncy, double z1, double z2, GC5 gc, int* flag, double* out,
                           cudaStream_t st);

@@ -1095,7 +1095,7 @@ cudaError_t with_plan(int L, int E, F&& f) {
     if (COL && L == 2000 && col_e10()) return f(Tag<SPlanG<double, 10, 40, 10, 10, 10, 2>>{});
     if (ROW && L == 2000 && row_e10()) return f(Tag<SPlanG<double, 10, 40, 10, 10, 10, 2>>{});
     switch (L) {
-      case 2048: return f(Tag<SPlan<double, 8, 8, 8, 8, 8, 4>>{});
+      case 2048: return f(Tag<SPlan<double, 16, 16, 16, 16, 8>>{});
       case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
       case 512: return f(Tag<SPlan<double, 8, 8, 8, 8, 8>>{});
       case 432: return f(Tag<SPlan<double, 12, 12, 12, 12, 3>>{});

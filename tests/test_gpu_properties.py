@@ -1,6 +1,6 @@
 """Size-independent properties at BASELINE sizes, where the oracle is too slow.
 
-Full C4 (1000x1000x128, 2000x2000 FFTs): adjoint identity, linearity, zero ->
+Full C4 (1000x1000x128, 2048x2048 FFTs of the 1999x1999 embedding): adjoint identity, linearity, zero ->
 zero, layer-shard additivity.  Adjoint bound as in pkg/tests/test_multiply.py:54-66.
 """
 import numpy as np

@@ -58,8 +58,31 @@ void run(int L, const int* radices, int npass, int ncols, int C, int reps) {
   }
   cudaMemcpy(tw, htw.data(), sizeof(V) * L, cudaMemcpyHostToDevice);
   cudaMemcpy(din, h.data(), sizeof(V) * h.size(), cudaMemcpyHostToDevice);
+  // per-pass twiddle tables (as capi.cu per_pass_table builds them)
+  std::vector<V> hp;
+  {
+    long ns = 1;
+    const int np = npass < 0 ? -npass : npass;
+    for (int p = 0; p < np; ++p) {
+      const int R = radices[p];
+      if (ns > 1)
+        for (int r = 1; r < R; ++r)
+          for (long k = 0; k < ns; ++k) {
+            long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)(r * k) / (ns * R);
+            V c;
+            c.x = (T)cosl(a);
+            c.y = (T)-sinl(a);
+            hp.push_back(c);
+          }
+      ns *= R;
+    }
+  }
+  V* twp;
+  cudaMalloc(&twp, sizeof(V) * (hp.size() + 1));
+  cudaMemcpy(twp, hp.data(), sizeof(V) * hp.size(), cudaMemcpyHostToDevice);
   FFTDesc<T> d;
   d.tw = tw;
+  d.twp = twp;
   d.L = L;
   d.nt = L / E;
   d.npass = npass < 0 ? -npass : npass;
@@ -106,14 +129,19 @@ void run(int L, const int* radices, int npass, int ncols, int C, int reps) {
   cudaFree(din);
   cudaFree(dout);
   cudaFree(tw);
+  cudaFree(twp);
 }
 
 int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 20;
   const int r20[] = {20, 20, 5};
-  using P20 = SPlanG<double, 20, 20, 20, 20, 5>;
-  run<P20, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
-  using F20 = SPlanG<float, 20, 80, 20, 20, 5>;
-  run<F20, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
+  const int r16[] = {16, 16, 8};
+  const int r8[] = {8, 8, 8, 4};
+  run<SPlan<double, 20, 20, 20, 20, 5>, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
+  run<SPlan<double, 16, 16, 16, 16, 8>, 128, 4>(2048, r16, -3, 1025 * 32, 1, reps);
+  run<SPlan<double, 16, 16, 16, 16, 8>, 256, 2>(2048, r16, -3, 1025 * 32, 2, reps);
+  run<SPlan<double, 8, 8, 8, 8, 8, 4>, 256, 2>(2048, r8, -4, 1025 * 32, 1, reps);
+  run<SPlan<float, 20, 80, 20, 20, 5>, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
+  run<SPlan<float, 16, 16, 16, 16, 8>, 128, 4>(2048, r16, -3, 1025 * 32, 1, reps);
   return 0;
 }
