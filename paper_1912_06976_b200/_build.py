@@ -40,7 +40,15 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, variant=None, defines=()):
+    """Build the library; ``variant``/``defines`` (development experiments)
+    build into build/<variant>/ with extra -D flags instead of in-tree; load
+    such a build with BTTB_LIB_PATH=build/<variant>/libbttb_sm100.so."""
+    global BUILD, LIB
+    if variant:
+        BUILD = os.path.join(ROOT, "build", variant)
+        LIB = os.path.join(BUILD, "libbttb_sm100.so")
+        force = True
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INC, "bttb_sm100.h"))
@@ -50,7 +58,7 @@ def build(force=False, verbose=False):
         obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + headers + [__file__]):
-            cmd = [nvcc()] + ARCH + COMMON + flags + ["-c", src, "-o", obj]
+            cmd = [nvcc()] + ARCH + COMMON + list(defines) + flags + ["-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
@@ -63,5 +71,7 @@ def build(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    print(build(force="--force" in args, verbose=True, variant=var,
+                defines=[a for a in args if a.startswith("-D")]))

@@ -10,7 +10,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbttb_sm100.so")
+# BTTB_LIB_PATH: a development build variant (paper_1912_06976_b200/_build.py --variant)
+LIB_PATH = os.environ.get("BTTB_LIB_PATH") or os.path.join(_HERE, "libbttb_sm100.so")
 
 BTTB_OK, BTTB_EINVAL, BTTB_ECUDA, BTTB_ENONFINITE, BTTB_ENOMEM = 0, -1, -2, -3, -4
 GRAVITY, MAGNETIC = 0, 1

@@ -1162,8 +1162,12 @@ template <class PL> struct Shape {
     return 2048 / (warps(threads) * regs) > 1 ? 2048 / (warps(threads) * regs) : 1;
   }
   // register targets: the column kernels keep E-element accumulators beside the data
+#ifdef COL_REGS_F64
+  static constexpr int col_regs = sizeof(T) == 4 ? COL_REGS_F32 : COL_REGS_F64;
+#else
   static constexpr int col_regs = sizeof(T) == 4 ? COL_REGS_F32
                                   : (64 + 4 * PL::E * 2 > 255 ? 255 : 64 + 4 * PL::E * 2);
+#endif
   static constexpr int col_regs_rounded =
       col_regs <= 96 ? 96 : col_regs <= 128 ? 128 : (col_regs <= 144 ? 144 : (col_regs <= 168 ? 168 : 255));
   // row passes hold E complex values plus the separated tile: fp32 needs far fewer registers
@@ -1447,7 +1451,8 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    if constexpr (PL::kStatic && PL::NT >= 32 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
+    // (whole-warp teams, e.g. 2048 with 128 threads, measured no gain: 4.18 vs 4.14 ms/step)
+    if constexpr (PL::kStatic && PL::NT >= 32 && PL::NT < 128 && PL::NT % 32 != 0 && sizeof(T) == 8 &&
                   (PL::E * 4) % 16 == 0) {
       if (tma_ok() && tmem_fwd_ok()) {
         auto kern = k_col_fwd_tmem<PL, 3>;
@@ -1496,7 +1501,8 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    if constexpr (PL::kStatic && PL::NT >= 32 && sizeof(T) == 8 && PL::NT % 32 != 0 &&
+    // (whole-warp teams, e.g. 2048 with 128 threads, measured no gain: 4.18 vs 4.14 ms/step)
+    if constexpr (PL::kStatic && PL::NT >= 32 && PL::NT < 128 && PL::NT % 32 != 0 && sizeof(T) == 8 &&
                   (PL::E * 4) % 16 == 0) {
       if (tma_ok() && tmem_tra_ok()) {
         auto kern = k_col_tra_tmem<PL, 3>;

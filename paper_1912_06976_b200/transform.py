@@ -37,10 +37,10 @@ class TransformStack:
 
     Attributes follow the reference ``TransformStack`` (transform.py:40-58):
     ``grid``, ``kind``, ``kernel_evals_per_layer`` and ``element_count`` (the
-    reference's count of stored complex values, nz*mx*my).  The per-layer
-    full-spectrum tuples ``forward`` / ``transpose`` of the reference are not
-    materialised: the device keeps (Hx, Ly) half spectra instead; use
-    :meth:`layer_spectrum`.
+    reference's count of stored complex values, nz*mx*my).  The device keeps
+    (Hx, Ly) half spectra at FFT lengths ``fft_shape`` (:meth:`layer_spectrum`);
+    the reference's full-spectrum tuples ``forward`` / ``transpose`` are
+    materialised on the host only when accessed.
     """
 
     def __init__(self, handle, grid, kind, dtype, device, layer_range, evals, params=None):
@@ -53,6 +53,7 @@ class TransformStack:
         self.device = device
         self.layer_begin, self.layer_end = layer_range
         self.kernel_evals_per_layer = evals
+        self._ref_stacks = None
         info = self.info()
         self.fft_shape = (int(info[0]), int(info[1]))
         self.spectrum_shape = (int(info[2]), int(info[1]))
@@ -66,12 +67,25 @@ class TransformStack:
 
     @property
     def forward(self):
-        raise NotImplementedError(
-            "the device cache holds (Hx, Ly) half spectra at FFT lengths "
-            f"{self.fft_shape}, not the reference's full (mx, my) arrays; "
-            "use layer_spectrum()")
+        """Reference-shaped forward stack: per local layer fft2(T^circ), (mx, my) complex128.
 
-    transpose = forward
+        A lazy HOST materialisation for API compatibility (transform.py:40-58,
+        :100-101), off the hot path: the GPU-generated window of each layer
+        is embedded at the minimal (mx, my) size (transform.py:85-88) and
+        transformed with numpy's FFT (lengths like 1999 are outside the device
+        FFT family).  Cached after the first access.  The device operator
+        never uses it.
+        """
+        if self._ref_stacks is None:
+            self._ref_stacks = _reference_stacks(self)
+        return self._ref_stacks[0]
+
+    @property
+    def transpose(self):
+        """Reference-shaped transpose stack: fft2(transpose_layout(T^circ)) per local layer."""
+        if self._ref_stacks is None:
+            self._ref_stacks = _reference_stacks(self)
+        return self._ref_stacks[1]
 
     # -- device plan ---------------------------------------------------------
     @property
@@ -169,86 +183,209 @@ def build_transform_stack(grid, params, dtype="float64", device=0, layers=None, 
 # ---------------------------------------------------------------------------
 _MAGIC = b"BTB2"
 _VERSION = 1
+_REF_MAGIC = b"BTTB"  # the reference's own layout (transform.py:19-22)
+_REF_VERSION = 1
 _KIND_CODES = {"gravity": 0, "magnetic": 1}
 _DTYPE_CODES = {"float64": 0, "float32": 1}
 
 
-def save_stack(stack, path):
-    """Persist a device stack: its half spectra as cached, plus what rebuilds the plan.
+def _embedding(window, sx, sy):
+    """T^circ of a response window at the minimal size (transform.py:85-88)."""
+    return np.roll(window[::-1, ::-1], (sx, sy), axis=(0, 1))
 
-    Little-endian layout: magic "BTB2" (not the reference's "BTTB": the payload
-    is the device cache, (Hx, Ly) half spectra at FFT lengths (Lx, Ly), scaled
-    by 1/(Lx*Ly), instead of two full complex128 (mx, my) stacks), version u32,
-    kind u8, dtype u8, grid counts 7 x i64, spacings 2 x f64, nz+1 depths,
-    gamma*scale f64, gc 5 x f64, kernel D, I, F 3 x f64, layer range 2 x i64,
-    Lx, Ly 2 x i64, then layer_end-layer_begin spectra.  Loading gives
-    bit-identical products (the spectra are not recomputed).
+
+def _window_from_embedding(T, sx, sy):
+    """Inverse of :func:`_embedding`: the response window a T^circ holds."""
+    return np.roll(T, (-sx, -sy), axis=(0, 1))[::-1, ::-1]
+
+
+def _reference_stacks(stack):
+    fw, tr = [], []
+    g = stack.grid
+    for r in range(stack.layer_begin, stack.layer_end):
+        T = _embedding(stack.layer_window(r), g.sx, g.sy)
+        fw.append(np.fft.fft2(T))
+        tr.append(np.fft.fft2(transpose_layout(T)))
+    return tuple(fw), tuple(tr)
+
+
+def save_stack(stack, path, format="native"):
+    """Persist a stack (transform.py:107-127).
+
+    ``format="native"`` (default): magic "BTB2" -- the device cache itself,
+    (Hx, Ly) half spectra at FFT lengths (Lx, Ly) scaled by 1/(Lx*Ly), plus
+    what rebuilds the plan.  Little-endian: magic, version u32, kind u8,
+    dtype u8, grid counts 7 x i64, spacings 2 x f64, nz+1 depths, gamma*scale
+    f64, gc 5 x f64, kernel D, I, F 3 x f64 (NaN when unknown), layer range
+    2 x i64, Lx, Ly 2 x i64, then layer_end-layer_begin spectra.  Loading
+    gives bit-identical products (nothing is recomputed).
+
+    ``format="reference"``: the reference's own "BTTB" v1 layout (full
+    complex128 fft2 of T^circ and of its transpose layout at (mx, my), every
+    layer), readable by the reference's ``load_stack``.  Written from the
+    GPU-generated windows through :attr:`TransformStack.forward`; needs a plan
+    holding all nz layers.
     """
+    if format == "reference":
+        return _save_reference(stack, path)
+    if format != "native":
+        raise ValueError(f"format must be 'native' or 'reference', got {format!r}")
     g = stack.grid
     p = stack.params
-    if p is None:
-        raise ValueError("stack has no kernel parameters to persist")
     lx, ly = stack.fft_shape
+    nan = float("nan")
     with open(path, "wb") as fh:
         fh.write(_MAGIC)
         fh.write(struct.pack("<IBB", _VERSION, _KIND_CODES[stack.kind], _DTYPE_CODES[str(stack.dtype)]))
         fh.write(struct.pack("<7q", g.sx, g.sy, g.nz, g.pxl, g.pxr, g.pyl, g.pyr))
         fh.write(struct.pack("<2d", g.dx, g.dy))
         fh.write(np.asarray(g.z_blocks, dtype="<f8").tobytes())
-        gc = list(p.gc) if p.kind == "magnetic" else [0.0] * 5
-        fh.write(struct.pack("<6d", p.gamma * p.scale, *gc))
-        fh.write(struct.pack("<3d", p.D, p.I, p.F))
+        if p is None:
+            fh.write(struct.pack("<6d", *([nan] * 6)))
+            fh.write(struct.pack("<3d", nan, nan, nan))
+        else:
+            gc = list(p.gc) if p.kind == "magnetic" else [0.0] * 5
+            fh.write(struct.pack("<6d", p.gamma * p.scale, *gc))
+            fh.write(struct.pack("<3d", p.D, p.I, p.F))
         fh.write(struct.pack("<4q", stack.layer_begin, stack.layer_end, lx, ly))
         for r in range(stack.nz_local):
             fh.write(np.ascontiguousarray(stack.layer_spectrum(r)).tobytes())
 
 
-def load_stack(path, device=0):
-    """Read back a stack written by :func:`save_stack` onto a device (no rebuild)."""
-    from .grid import make_grid
+def _save_reference(stack, path):
+    g = stack.grid
+    if (stack.layer_begin, stack.layer_end) != (0, g.nz):
+        raise ValueError("the reference stack format holds every layer; this plan holds layers "
+                         f"[{stack.layer_begin}, {stack.layer_end}) of {g.nz}")
+    mx, my = g.embed_shape
+    with open(path, "wb") as fh:
+        fh.write(_REF_MAGIC)
+        fh.write(struct.pack("<IB", _REF_VERSION, _KIND_CODES[stack.kind]))
+        fh.write(struct.pack("<7q", g.sx, g.sy, g.nz, g.pxl, g.pxr, g.pyl, g.pyr))
+        fh.write(struct.pack("<2d", g.dx, g.dy))
+        fh.write(np.asarray(g.z_blocks, dtype="<f8").tobytes())
+        fh.write(struct.pack("<3q", g.nz, mx, my))
+        for arr in stack.forward + stack.transpose:
+            fh.write(np.ascontiguousarray(arr, dtype="<c16").tobytes())
+
+
+def _native_params(kind, gs, gc, D, I, F):  # noqa: E741
     from .kernels import GRAVITATIONAL_CONST, KernelParams
 
+    if not np.isfinite(gs):
+        return None
+    if kind == "gravity":
+        return KernelParams(kind="gravity", gamma=GRAVITATIONAL_CONST, scale=gs / GRAVITATIONAL_CONST)
+    return KernelParams(kind="magnetic", D=D, I=I, F=F, gc=tuple(gc))
+
+
+def _grid_struct(grid):
+    zc = np.ascontiguousarray(grid.z_blocks, dtype=float)
+    return _lib.BttbGrid(grid.sx, grid.sy, grid.nz, grid.pxl, grid.pxr, grid.pyl, grid.pyr,
+                         grid.dx, grid.dy, _lib.as_dptr(zc)), zc
+
+
+def load_stack(path, device=0, dtype=None):
+    """Read back a persisted stack onto a device (transform.py:130-159).
+
+    Native "BTB2" files upload their cached spectra (no rebuild; ``dtype``
+    must be None or the file's).  Reference "BTTB" files (the reference's
+    ``save_stack`` output) are accepted too: each layer's T^circ is recovered
+    on the host as real(ifft2(forward[r])) -- a format conversion, off the
+    hot path -- and the GPU rebuilds the spectra from those windows
+    (``bttb_plan_create_from_windows``) at the plan's FFT lengths, in
+    ``dtype`` (default "float64").  Error messages follow the reference
+    ("magic", "unsupported stack version", "inconsistent", "truncated").
+    """
     with open(path, "rb") as fh:
         magic = fh.read(4)
-        if magic == b"BTTB":
-            raise ValueError("reference-format stack file (full complex128 spectra at the "
-                             "minimal embedding): rebuild it with build_transform_stack")
+        if magic == _REF_MAGIC:
+            return _load_reference(fh, device, dtype or "float64")
         if magic != _MAGIC:
             raise ValueError(f"not a transform-stack file (magic {magic!r})")
-        version, kind_code, dt_code = struct.unpack("<IBB", fh.read(6))
-        if version != _VERSION:
-            raise ValueError(f"unsupported stack version {version}")
-        sx, sy, nz, pxl, pxr, pyl, pyr = struct.unpack("<7q", fh.read(56))
-        dx, dy = struct.unpack("<2d", fh.read(16))
-        z = np.frombuffer(fh.read(8 * (nz + 1)), dtype="<f8")
-        gs, *gc = struct.unpack("<6d", fh.read(48))
-        D, I, F = struct.unpack("<3d", fh.read(24))  # noqa: E741
-        lo, hi, lx, ly = struct.unpack("<4q", fh.read(32))
-        grid = make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, z)
-        kind = {0: "gravity", 1: "magnetic"}[kind_code]
-        dtype = {0: "float64", 1: "float32"}[dt_code]
-        hx = lx // 2 + 1
-        cdt = np.dtype("<c16" if dtype == "float64" else "<c8")
-        count = (hi - lo) * hx * ly
-        buf = fh.read(count * cdt.itemsize)
-        if len(buf) != count * cdt.itemsize:
-            raise ValueError("truncated transform-stack file")
+        return _load_native(fh, device, dtype)
+
+
+def _load_native(fh, device, want_dtype):
+    from .grid import make_grid
+
+    head = fh.read(6)
+    if len(head) != 6:
+        raise ValueError("truncated transform-stack file")
+    version, kind_code, dt_code = struct.unpack("<IBB", head)
+    if version != _VERSION:
+        raise ValueError(f"unsupported stack version {version}")
+    sx, sy, nz, pxl, pxr, pyl, pyr = struct.unpack("<7q", fh.read(56))
+    dx, dy = struct.unpack("<2d", fh.read(16))
+    z = np.frombuffer(fh.read(8 * (nz + 1)), dtype="<f8")
+    gs, *gc = struct.unpack("<6d", fh.read(48))
+    D, I, F = struct.unpack("<3d", fh.read(24))  # noqa: E741
+    lo, hi, lx, ly = struct.unpack("<4q", fh.read(32))
+    grid = make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, z)
+    kind = {0: "gravity", 1: "magnetic"}[kind_code]
+    dtype = {0: "float64", 1: "float32"}[dt_code]
+    if want_dtype is not None and want_dtype != dtype:
+        raise ValueError(f"stack file holds {dtype} spectra, {want_dtype} requested")
+    hx = lx // 2 + 1
+    cdt = np.dtype("<c16" if dtype == "float64" else "<c8")
+    count = (hi - lo) * hx * ly
+    buf = fh.read(count * cdt.itemsize)
+    if len(buf) != count * cdt.itemsize:
+        raise ValueError("truncated transform-stack file")
     spectra = np.frombuffer(buf, dtype=cdt)
-    if kind == "gravity":
-        params = KernelParams(kind="gravity", gamma=GRAVITATIONAL_CONST, scale=gs / GRAVITATIONAL_CONST)
-    else:
-        params = KernelParams(kind="magnetic", D=D, I=I, F=F, gc=tuple(gc))
-    zc = np.ascontiguousarray(grid.z_blocks, dtype=float)
-    g = _lib.BttbGrid(grid.sx, grid.sy, grid.nz, grid.pxl, grid.pxr, grid.pyl, grid.pyr,
-                      grid.dx, grid.dy, _lib.as_dptr(zc))
-    k = params.native()
-    if kind == "gravity":
-        k.gamma_scaled = gs  # exactly the persisted multiplier
+    params = _native_params(kind, gs, gc, D, I, F)
+    g, _z = _grid_struct(grid)
+    k = _lib.BttbKernel(_lib.GRAVITY if kind == "gravity" else _lib.MAGNETIC,
+                        gs if np.isfinite(gs) else 0.0, (_lib.ctypes.c_double * 5)(*gc))
     h = _lib.ctypes.c_void_p()
     _lib.check(_lib.lib().bttb_plan_create_from_spectra(
         _lib.ctypes.byref(h), _lib.ctypes.byref(g), _lib.ctypes.byref(k), _DTYPES[dtype], int(device),
         lo, hi, lx, ly, spectra.ctypes.data_as(_lib.ctypes.c_void_p)))
     return TransformStack(h, grid, kind, dtype, int(device), (lo, hi), 0, params)
+
+
+def _load_reference(fh, device, dtype):
+    from .grid import make_grid
+
+    if dtype not in _DTYPES:
+        raise ValueError(f"dtype must be one of {sorted(_DTYPES)}, got {dtype!r}")
+    head = fh.read(5)
+    if len(head) != 5:
+        raise ValueError("truncated transform-stack file")
+    version, kind_code = struct.unpack("<IB", head)
+    if version != _REF_VERSION:
+        raise ValueError(f"unsupported stack version {version}")
+    if kind_code not in (0, 1):
+        raise ValueError(f"unknown kernel kind code {kind_code}")
+    sx, sy, nz, pxl, pxr, pyl, pyr = struct.unpack("<7q", fh.read(56))
+    dx, dy = struct.unpack("<2d", fh.read(16))
+    z = np.frombuffer(fh.read(8 * (nz + 1)), dtype="<f8")
+    layers, mx, my = struct.unpack("<3q", fh.read(24))
+    grid = make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, z)
+    if (mx, my) != grid.embed_shape or layers != nz:
+        raise ValueError("stack header is inconsistent with its grid")
+    count = mx * my
+    windows = np.empty((nz, mx, my))
+    for r in range(nz):
+        buf = fh.read(16 * count)
+        if len(buf) != 16 * count:
+            raise ValueError("truncated transform-stack file")
+        F = np.frombuffer(buf, dtype="<c16").reshape(mx, my)
+        windows[r] = _window_from_embedding(np.fft.ifft2(F).real, sx, sy)
+    # the transpose stack is conj(forward) for a real T^circ; it is read only
+    # to keep the reference's truncation semantics
+    for _ in range(nz):
+        if len(fh.read(16 * count)) != 16 * count:
+            raise ValueError("truncated transform-stack file")
+    kind = {0: "gravity", 1: "magnetic"}[kind_code]
+    g, _z = _grid_struct(grid)
+    k = _lib.BttbKernel(_lib.GRAVITY if kind == "gravity" else _lib.MAGNETIC, 0.0,
+                        (_lib.ctypes.c_double * 5)())
+    h = _lib.ctypes.c_void_p()
+    _lib.check(_lib.lib().bttb_plan_create_from_windows(
+        _lib.ctypes.byref(h), _lib.ctypes.byref(g), _lib.ctypes.byref(k), _DTYPES[dtype], int(device),
+        0, nz, 0, 0, _lib.as_dptr(windows)))
+    return TransformStack(h, grid, kind, dtype, int(device), (0, nz), 0, None)
 
 
 def transpose_layout(T):

@@ -96,7 +96,18 @@ def c4_layers():
     np.savez_compressed(os.path.join(HERE, "C4_windows.npz"), **out)
 
 
+def stack_files():
+    """Reference-format stack files (the reference's own save_stack) of the
+    6x5x2 grid padded (2, 1, 1, 2); products are in small_6x5x2.npz."""
+    from bttb.transform import save_stack
+
+    for params in (GRAV, MAG):
+        g = bttb.make_grid(6, 5, 2, 2, 1, 1, 2, 1.0, 1.5, (0.0, 1.0, 2.5))
+        save_stack(bttb.build_transform_stack(g, params), os.path.join(HERE, f"ref_stack_{params.kind}.bttb"))
+
+
 if __name__ == "__main__":
+    stack_files()
     small_cases()
     config_case("C1")
     config_case("C2")

@@ -4,6 +4,8 @@ Mirrors the reference's tests of these contracts (pkg/tests/test_cli.py:105-217,
 pkg/tests/test_transform.py:144-176, test_acceptance.py:185-198) on the
 drop-in; CPU tests need no GPU, the rest are marked gpu.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -155,8 +157,103 @@ def test_bad_magic_and_reference_format(tmp_path):
         B.load_stack(str(junk))
     ref = tmp_path / "ref.bttb"
     ref.write_bytes(b"BTTB" + b"\0" * 64)
-    with pytest.raises(ValueError, match="reference-format"):
+    with pytest.raises(ValueError, match="unsupported stack version 0"):
         B.load_stack(str(ref))
+
+
+REF_FILES = {"gravity": "ref_stack_gravity.bttb", "magnetic": "ref_stack_magnetic.bttb"}
+REF_KEYS = {"gravity": "gravity_2_1_1_2", "magnetic": "magnetic_2_1_1_2"}
+
+
+def _golden_path(name):
+    from conftest import GOLDEN
+    return os.path.join(GOLDEN, name)
+
+
+@pytest.mark.parametrize("kind", ["gravity", "magnetic"])
+def test_reference_file_truncated_or_inconsistent(tmp_path, kind):
+    """Reference-format errors are raised while parsing (no GPU needed)."""
+    data = open(_golden_path(REF_FILES[kind]), "rb").read()
+    cut = tmp_path / "cut.bttb"
+    cut.write_bytes(data[:-8])
+    with pytest.raises(ValueError, match="truncated"):
+        B.load_stack(str(cut))
+    # header (magic 4 + version/kind 5 + 7 counts 56 + spacings 16 + 3 depths 24) then layer count
+    off = 4 + 5 + 56 + 16 + 24
+    bad = bytearray(data)
+    bad[off:off + 8] = (5).to_bytes(8, "little")
+    badp = tmp_path / "bad.bttb"
+    badp.write_bytes(bytes(bad))
+    with pytest.raises(ValueError, match="inconsistent"):
+        B.load_stack(str(badp))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("kind", ["gravity", "magnetic"])
+def test_load_reference_format_file(golden, kind, dtype):
+    """A stack file written by the REFERENCE's save_stack loads and reproduces
+    the reference's own products (tests/golden/make_golden.py stack_files)."""
+    z = golden("small_6x5x2.npz")
+    key = REF_KEYS[kind]
+    u, v = z[f"{key}/u"], z[f"{key}/v"]
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    with B.load_stack(_golden_path(REF_FILES[kind]), dtype=dtype) as st:
+        assert st.kind == kind and st.dtype == np.dtype(dtype) and st.params is None
+        assert st.grid == B.make_grid(6, 5, 2, 2, 1, 1, 2, 1.0, 1.5, (0.0, 1.0, 2.5))
+        uq = u.astype(dtype).astype(float)
+        vq = v.astype(dtype).astype(float)
+        g = O.ogrid(6, 5, 2, 2, 1, 1, 2, 1.0, 1.5, (0.0, 1.0, 2.5))
+        fw, tr = O.build_spectra(g, kind, O.grav_constants() if kind == "gravity"
+                                 else O.mag_constants(33.0, 47.0, 45000.0))
+        ref_f = z[f"{key}/fwd"] if dtype == "float64" else O.forward(g, fw, uq)
+        ref_t = z[f"{key}/tra"] if dtype == "float64" else O.transpose(g, tr, vq)
+        assert O.rel_l2(ref_f, B.apply(st, u, "forward")) <= tol
+        assert O.rel_l2(ref_t, B.apply(st, v, "transpose")) <= tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("params", [B.KernelParams.gravity(), B.KernelParams.magnetic(33.0, 47.0, 45000.0)],
+                         ids=["gravity", "magnetic"])
+def test_save_reference_format_and_lazy_spectra(tmp_path, params):
+    """save_stack(format="reference") writes the reference layout: its arrays
+    equal the oracle's fft2(T^circ) / fft2(transpose layout); the lazy
+    TransformStack.forward/.transpose are the same arrays; the file loads back."""
+    g = B.make_grid(7, 5, 3, 1, 2, 2, 0, 1.0, 1.5, (0.0, 1.0, 2.5, 4.0))
+    og = O.ogrid(7, 5, 3, 1, 2, 2, 0, 1.0, 1.5, (0.0, 1.0, 2.5, 4.0))
+    consts = O.grav_constants() if params.kind == "gravity" else O.mag_constants(33.0, 47.0, 45000.0)
+    fw, tr = O.build_spectra(og, params.kind, consts)
+    path = str(tmp_path / "ref.bttb")
+    rng = np.random.default_rng(8)
+    u, v = rng.uniform(size=g.n), rng.uniform(size=g.m)
+    with B.build_transform_stack(g, params) as st:
+        assert len(st.forward) == g.nz and sum(a.size for a in st.forward) == st.element_count
+        for r in range(g.nz):
+            scale = np.abs(fw[r]).max()
+            assert np.abs(st.forward[r] - fw[r]).max() <= 1e-13 * scale
+            assert np.abs(st.transpose[r] - tr[r]).max() <= 1e-13 * scale
+        B.save_stack(st, path, format="reference")
+        f0, t0 = B.apply(st, u, "forward"), B.apply(st, v, "transpose")
+    mx, my = g.embed_shape
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"BTTB"
+    head = 4 + 5 + 56 + 16 + 8 * (g.nz + 1) + 24
+    arrs = np.frombuffer(raw[head:], dtype="<c16").reshape(2, g.nz, mx, my)
+    for r in range(g.nz):
+        scale = np.abs(fw[r]).max()
+        assert np.abs(arrs[0, r] - fw[r]).max() <= 1e-13 * scale
+        assert np.abs(arrs[1, r] - tr[r]).max() <= 1e-13 * scale
+    with B.load_stack(path) as ld:
+        assert O.rel_l2(f0, B.apply(ld, u, "forward")) <= 1e-13
+        assert O.rel_l2(t0, B.apply(ld, v, "transpose")) <= 1e-13
+
+
+@pytest.mark.gpu
+def test_save_reference_format_needs_every_layer(tmp_path):
+    g = B.make_grid(6, 5, 4, 1, 1, 1, 1, 1.0, 1.5, (0.0, 1.0, 2.5, 3.0, 4.0))
+    with B.build_transform_stack(g, B.KernelParams.gravity(), layers=(1, 3)) as st:
+        with pytest.raises(ValueError, match="every layer"):
+            B.save_stack(st, str(tmp_path / "x.bttb"), format="reference")
 
 
 @pytest.mark.gpu
@@ -169,3 +266,15 @@ def test_truncated_stack(tmp_path):
     path.write_bytes(data[:-8])
     with pytest.raises(ValueError, match="truncated"):
         B.load_stack(str(path))
+
+
+@pytest.mark.gpu
+def test_cli_reference_format_round_trip(tmp_path):
+    path, vec, out = str(tmp_path / "r.bttb"), str(tmp_path / "u.bin"), str(tmp_path / "d.bin")
+    assert main(["build-stack", *GRID_FLAGS, "--format", "reference", "--out", path]) == 0
+    assert open(path, "rb").read(4) == b"BTTB"
+    u = np.random.default_rng(12).uniform(size=GRID.n)
+    B.write_vector(u, vec)
+    assert main(["apply", "--stack", path, "--in", vec, "--mode", "forward", "--out", out]) == 0
+    with B.build_transform_stack(GRID, B.KernelParams.gravity()) as st:
+        assert O.rel_l2(B.apply(st, u, "forward"), B.read_vector(out)) <= 1e-13
