@@ -284,6 +284,7 @@ struct bttb_plan_s {
   void* window_base = nullptr;
   size_t window_bytes = 0;
   int64_t last_K = 0, last_G = 0, last_launches = 0;
+  int* pipe_err_host = nullptr;  // pinned copy of the fused pipeline's deadlock-guard flag
   std::mutex mu;
 
   int64_t n_r() const { return nx * ny; }
@@ -488,8 +489,149 @@ int set_l2_window(bttb_plan_s* p, void* base, size_t bytes) {
   return BTTB_OK;
 }
 
+// Fused layer pipeline (pipeline.cuh), square FFT lengths with a pipeline
+// plan: per vector, forward = pipeline kernel + row C2R of the stations;
+// transpose = row R2C of the data + pipeline kernel.  Workspace: the ring of
+// two layer intermediates, the station half spectrum W, the counters.
+template <class T>
+int run_pipe(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st) {
+  using V = cplx<T>;
+  const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
+  const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
+                nloc = p->nloc();
+  if (p->pipe_err_host && *p->pipe_err_host)
+    return fail(BTTB_ECUDA, "fused pipeline deadlock guard tripped in an earlier apply");
+  if (!p->pipe_err_host) CU(cudaMallocHost(&p->pipe_err_host, sizeof(int)));
+  static const int nb_env = getenv("BTTB_PIPE_NB") ? atoi(getenv("BTTB_PIPE_NB")) : 3;
+  const int NB = std::max(2, nb_env);  // ring slots (>= 2: see pipeline.cuh)
+  const size_t ring = round_up((size_t)NB * Hx * ny * sizeof(V), 4096);
+  const size_t wbytes = round_up((size_t)Hx * sy * sizeof(V), 4096);
+  const int ncnt = pipe_counter_ints((int)p->nzl);
+  const size_t cbytes = (size_t)ncnt * sizeof(int);
+  // BTTB_PIPE_STATS=1: per-team cycle accounting printed to stderr (development aid)
+  static const bool stats_on = getenv("BTTB_PIPE_STATS") && atoi(getenv("BTTB_PIPE_STATS")) != 0;
+  const size_t sbytes = stats_on ? (size_t)8 * pipe_grid() * pipe_teams() * sizeof(long long) : 0;
+  int rc;
+  if ((rc = p->work.ensure(ring + wbytes + round_up(cbytes, 4096) + sbytes))) return rc;
+  char* base = static_cast<char*>(p->work.p);
+  V* Wb = reinterpret_cast<V*>(base + ring);
+  int* cnt = reinterpret_cast<int*>(base + ring + wbytes);
+  long long* stats = stats_on ? reinterpret_cast<long long*>(base + ring + wbytes + round_up(cbytes, 4096)) : nullptr;
+  CU(cudaMemsetAsync(cnt, 0, cbytes, st));  // counters and the err flag (last int)
+  PipeArgs a{};
+  a.S = p->spectra;
+  a.s_rstride = (long long)Hx * p->Ly;
+  a.lds = (int)p->Ly;
+  a.ring = base;
+  a.ring_sstride = (long long)Hx * ny;
+  a.nb = NB;
+  a.sync = cnt;
+  a.nz = (int)p->nzl;
+  a.nx = (int)nx;
+  a.ny = (int)ny;
+  a.sy = (int)sy;
+  a.Hx = (int)Hx;
+  a.n_r = n_r;
+  a.stats = stats;
+  p->last_K = p->nzl;
+  p->last_G = 1;
+  int64_t launches = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    if (b > 0) CU(cudaMemsetAsync(cnt, 0, cbytes - sizeof(int), st));
+    if (mode == BTTB_FORWARD) {
+      a.in = static_cast<const T*>(x) + b * nloc;
+      a.out = Wb;
+      CU(launch_pipe<T>(0, a, dy, st));
+      RowC2RArgs oa{};
+      oa.in = Wb;
+      oa.in_sstride = (long long)Hx * sy;
+      oa.ld_in = (int)sy;
+      oa.nrows = (int)sy;
+      oa.Hx = (int)Hx;
+      oa.nslabs = 1;
+      oa.out = static_cast<T*>(y) + b * m;
+      oa.out_bstride = m;
+      oa.out_sstride = 0;
+      oa.spb = 1;
+      oa.ld_out = (int)sx;
+      oa.nout = (int)sx;
+      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
+    } else {
+      RowR2CArgs ra{};
+      ra.in = static_cast<const T*>(x) + b * m;
+      ra.in_bstride = m;
+      ra.in_sstride = 0;
+      ra.spb = 1;
+      ra.ld_in = (int)sx;
+      ra.nrows = (int)sy;
+      ra.nvalid = (int)sx;
+      ra.nslabs = 1;
+      ra.out = Wb;
+      ra.out_sstride = (long long)Hx * sy;
+      ra.ld_out = (int)sy;
+      ra.Hx = (int)Hx;
+      CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
+      a.in = Wb;
+      a.out = static_cast<T*>(y) + b * nloc;
+      CU(launch_pipe<T>(1, a, dy, st));
+    }
+    launches += 2;
+  }
+  CU(cudaMemcpyAsync(p->pipe_err_host, cnt + ncnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (stats_on) {  // last vector's accounting
+    const int n = pipe_grid() * pipe_teams();
+    std::vector<long long> hs((size_t)8 * n);
+    CU(cudaMemcpyAsync(hs.data(), stats, sbytes, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    {
+      int nzero = 0;
+      std::string ids;
+      for (int i = 0; i < n; ++i)
+        if (hs[8 * i + 6] == 0) {
+          if (nzero++ < 12) ids += " " + std::to_string(i);
+        }
+      if (nzero) fprintf(stderr, "[pipe] %d of %d teams wrote no stats:%s\n", nzero, n, ids.c_str());
+    }
+    double acc[6] = {0, 0, 0, 0, 0, 0}, mx[6] = {0, 0, 0, 0, 0, 0};
+    long long g0 = hs[6], g1 = hs[7];
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < 6; ++j) {
+        acc[j] += (double)hs[8 * i + j];
+        mx[j] = std::max(mx[j], (double)hs[8 * i + j]);
+      }
+      g0 = std::min(g0, hs[8 * i + 6]);
+      g1 = std::max(g1, hs[8 * i + 7]);
+    }
+    // start / end offsets (us) of the teams relative to the first start
+    std::vector<double> so(n), eo(n);
+    for (int i = 0; i < n; ++i) {
+      so[i] = (hs[8 * i + 6] - g0) * 1e-3;
+      eo[i] = (hs[8 * i + 7] - g0) * 1e-3;
+    }
+    std::sort(so.begin(), so.end());
+    std::sort(eo.begin(), eo.end());
+    fprintf(stderr,
+            "[pipe %s] span %.1f us; start offsets med/max %.1f/%.1f us; ends min/med/max %.1f/%.1f/%.1f us; per team "
+            "mean/max cycles: total %.0f/%.0f, wait %.0f/%.0f, rows %.0f/%.0f (%.1f items), cols %.0f/%.0f (%.1f items)\n",
+            mode == BTTB_FORWARD ? "fwd" : "tra", (g1 - g0) * 1e-3, so[n / 2], so[n - 1], eo[0], eo[n / 2], eo[n - 1],
+            acc[5] / n, mx[5], acc[0] / n, mx[0], acc[1] / n, mx[1], acc[3] / n, acc[2] / n, mx[2], acc[4] / n);
+  }
+  p->last_launches = launches;
+  return BTTB_OK;
+}
+
+// the fused pipeline runs square lengths >= BTTB_PIPE_MIN_L (default 1024;
+// smaller stacks fit L2 and batch better in the staged path); BTTB_PIPE=0 off
+bool use_pipe(const bttb_plan_s* p) {
+  static const int64_t min_l = getenv("BTTB_PIPE_MIN_L") ? atoll(getenv("BTTB_PIPE_MIN_L")) : 1024;
+  if (p->Lx != p->Ly || p->Lx < min_l) return false;
+  return p->dtype == BTTB_F64 ? pipe_supported<double>((int)p->Lx, (int)p->Hx)
+                              : pipe_supported<float>((int)p->Lx, (int)p->Hx);
+}
+
 template <class T>
 int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st) {
+  if (use_pipe(p)) return run_pipe<T>(p, mode, x, y, batch, st);
   using V = cplx<T>;
   const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
   const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
@@ -673,6 +815,7 @@ void destroy_plan(bttb_plan_s* p) {
   if (!p) return;
   DeviceGuard g(p->device);
   if (p->spectra) cudaFree(p->spectra);
+  if (p->pipe_err_host) cudaFreeHost(p->pipe_err_host);
   p->fx.release();
   p->fy.release();
   p->work.release();
@@ -858,6 +1001,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   if (where == BTTB_HOST_PTR) {
     CU(cudaMemcpyAsync(y, yd, out_elems * esz, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (p->pipe_err_host && *p->pipe_err_host) return fail(BTTB_ECUDA, "fused pipeline deadlock guard tripped");
   }
   return BTTB_OK;
 }

@@ -334,25 +334,39 @@ struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
 
+// Barrier of the exchanges: the whole CTA (default) or one team of a CTA that
+// runs several independent teams (named barrier `id`, `n` threads).
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct TeamSync {
+  int id, n;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  }
+};
+
 // hook() runs once, before the first exchange's barrier (e.g. to wait for an
 // asynchronous copy that still reads the exchange buffer)
 // PP: tw is the per-pass table block (OFF = this pass's offset in it);
 // otherwise tw is the length-L table.
-template <class T, int E, int L, int PAD, bool PP, int OFF, int NS, int R, int... Rest, class Hook = NoHook>
+template <class T, int E, int L, int PAD, bool PP, int OFF, int NS, int R, int... Rest, class Hook = NoHook,
+          class Sync = CtaSync>
 __device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
-                                     bool active = true, Hook hook = Hook{}) {
+                                     bool active = true, Hook hook = Hook{}, Sync sync = Sync{}) {
   constexpr int NT = L / E;
   static_assert(E % R == 0, "radix must divide elements per thread");
   spass_compute<T, E, R, NS, NT, L, PP>(v, active ? t : 0, PP ? tw + OFF : tw);
   if constexpr (sizeof...(Rest) > 0) {
     if constexpr (NS == 1) hook();
-    __syncthreads();
+    sync();
     spass_store<T, E, R, NS, NT, PAD>(v, sm, t, active);
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int s = 0; s < E; ++s)
       if (active) v[s] = sm[pad_slot<PAD>(t + NT * s)];
-    sfft<T, E, L, PAD, PP, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R, Rest...>(v, sm, t, tw, active);
+    sfft<T, E, L, PAD, PP, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R, Rest...>(v, sm, t, tw, active, NoHook{},
+                                                                                  sync);
   }
 }
 
@@ -392,6 +406,11 @@ struct SPlanT {
   __device__ __forceinline__ static void fft_hook(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
                                                   Hook hook) {
     sfft<T, E_, L, PAD, PP, 0, 1, Rs...>(v, sm, t, table(d), true, hook);
+  }
+  // one team of a multi-team CTA: exchanges synchronise on the team's barrier
+  __device__ __forceinline__ static void fft_team(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
+                                                  bool active, TeamSync sync) {
+    sfft<T, E_, L, PAD, PP, 0, 1, Rs...>(v, sm, t, table(d), active, NoHook{}, sync);
   }
 };
 

@@ -1147,6 +1147,10 @@ int static_radices(int L, bool fp64, int* out) {
   return n;
 }
 
+}  // namespace bttb
+#include "pipeline.cuh"
+namespace bttb {
+
 // Fixed launch shapes of the compile-time plans: teams per CTA and the
 // register target that sets __launch_bounds__ min-blocks (fp64 column kernels
 // keep an E-element accumulator, hence the larger budget).
@@ -1554,6 +1558,84 @@ cudaError_t launch_col_spec(const ColSpecArgs& a, const FFTDesc<double>& d, int 
     return cudaGetLastError();
   });
 }
+
+// ---------------------------------------------------------------------------
+// Fused layer pipeline launchers (pipeline.cuh)
+// ---------------------------------------------------------------------------
+#ifndef PIPE_TEAMS
+#define PIPE_TEAMS 3  // teams (128 threads each) per persistent CTA
+#endif
+
+int pipe_grid() { return sm_count(); }
+int pipe_teams() { return PIPE_TEAMS; }
+int pipe_counter_ints(int nz) { return pipe_err_index(nz, sm_count()) + 1; }
+
+// opt-in (BTTB_PIPE=1): correct (tests/test_gpu_pipeline.py) but measured
+// slower than the staged kernels on C4 fp64 at 2048^2 -- 5.74 vs 4.14 ms/step
+// with a 3-slot ring: its column/row items cost ~2.0 vs ~1.55 us of SM time,
+// as three teams per SM without shared memory for TMA double buffering leave
+// the L2 latency of every item exposed.
+bool pipe_enabled() {
+  static const bool on = env_flag("BTTB_PIPE", false);
+  return on;
+}
+
+template <class PL> constexpr bool pipe_plan() {
+  if constexpr (PL::kStatic) {
+    return PL::NT >= 64 && PL::NT <= pipe::TT && (PL::E * pipe::Words<cplx<typename PL::Scalar>>::W) % 16 == 0;
+  } else {
+    return false;
+  }
+}
+
+template <class T>
+bool pipe_supported(int L, int Hx) {
+  if (!pipe_enabled()) return false;
+  bool ok = false;
+  with_plan<T>(L, 0, [&](auto tag) {
+    using PL = typename decltype(tag)::type;
+    if constexpr (pipe_plan<PL>()) {
+      const int G = sm_count();
+      const int per_cta = (Hx + G - 1) / G;
+      ok = per_cta * pipe::Cfg<PL>::COLS <= 512;
+    }
+    return cudaSuccess;
+  });
+  return ok;
+}
+
+template <class T>
+cudaError_t launch_pipe(int mode, const PipeArgs& a, const FFTDesc<T>& d, cudaStream_t st) {
+  return with_plan<T>(d.L, 0, [&](auto tag) -> cudaError_t {
+    using PL = typename decltype(tag)::type;
+    if constexpr (pipe_plan<PL>()) {
+      using C = pipe::Cfg<PL>;
+      constexpr int TEAMS = PIPE_TEAMS;
+      const void* kern = mode == 0 ? (const void*)k_pipe_fwd<PL, TEAMS> : (const void*)k_pipe_tra<PL, TEAMS>;
+      // at least 120 KB of shared memory: exactly one CTA per SM (each allocates all of TMEM)
+      size_t smem = (size_t)TEAMS * C::team_slots() * sizeof(cplx<T>) + (size_t)(a.nz + 1) * sizeof(int);
+      if (smem < 120 * 1024) smem = 120 * 1024;
+      if (smem > 227 * 1024) return cudaErrorNotSupported;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      int nb = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TEAMS * pipe::TT, smem);
+      if (e != cudaSuccess) return e;
+      if (nb < 1) return cudaErrorCooperativeLaunchTooLarge;
+      PipeArgs args = a;
+      FFTDesc<T> dd = d;
+      void* params[2] = {&args, &dd};
+      return cudaLaunchCooperativeKernel(kern, dim3(sm_count()), dim3(TEAMS * pipe::TT), params, smem, st);
+    } else {
+      return cudaErrorNotSupported;
+    }
+  });
+}
+
+template bool pipe_supported<double>(int, int);
+template bool pipe_supported<float>(int, int);
+template cudaError_t launch_pipe<double>(int, const PipeArgs&, const FFTDesc<double>&, cudaStream_t);
+template cudaError_t launch_pipe<float>(int, const PipeArgs&, const FFTDesc<float>&, cudaStream_t);
 
 template cudaError_t launch_row_r2c<double>(const RowR2CArgs&, const FFTDesc<double>&, int, cudaStream_t);
 template cudaError_t launch_row_r2c<float>(const RowR2CArgs&, const FFTDesc<float>&, int, cudaStream_t);

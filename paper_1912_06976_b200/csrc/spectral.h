@@ -83,4 +83,31 @@ template <class TS> cudaError_t launch_col_spec(const ColSpecArgs& a, const FFTD
 // radix sequence of the registered compile-time plan of (L, dtype), 0 if none
 int static_radices(int L, bool fp64, int* out);
 
+// Fused layer pipeline (pipeline.cuh): one persistent cooperative kernel per
+// application and vector.  Forward: in = model (layer-major, rows of nx, n_r
+// per layer), out = W[kx][j < sy] (the column-inverse-transformed station
+// half spectrum; a row C2R pass finishes it).  Transpose: in = D[kx][j < sy]
+// (row R2C of the data), out = model.  ring: nb >= 2 slots [kx][q < ny] of
+// ring_sstride complex; sync: pipe_counter_ints(nz) zeroed ints.
+struct PipeArgs {
+  const void* in;
+  void* out;
+  const void* S;
+  long long s_rstride;
+  int lds;
+  void* ring;
+  long long ring_sstride;
+  int nb;
+  int* sync;
+  int nz, nx, ny, sy, Hx;
+  long long n_r;
+  long long* stats;  // optional per-team cycle accounting (6 x teams x grid), or null
+};
+int pipe_grid();   // CTAs of the pipeline kernels (one per SM)
+int pipe_teams();  // teams per CTA
+int pipe_counter_ints(int nz);  // ints of PipeArgs::sync (the err flag is the last)
+// true if the fused pipeline runs this length (square plans only) and dtype
+template <class T> bool pipe_supported(int L, int Hx);
+template <class T> cudaError_t launch_pipe(int mode, const PipeArgs& a, const FFTDesc<T>& d, cudaStream_t st);
+
 }  // namespace bttb
