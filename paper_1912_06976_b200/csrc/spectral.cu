@@ -824,9 +824,12 @@ template <class PL> struct RowTile {
   }
 };
 
-template <class PL, int MAXT, int MINB, int TEAMS>
+// QUAD (two teams): the CTA's four rows leave as ONE [kx][4 rows] box, so the
+// box rows are 32 bytes in fp32 (full L2 sectors) instead of 16.
+template <class PL, int MAXT, int MINB, int TEAMS, bool QUAD = false>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_r2c_t2d(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap omap) {
+  static_assert(!QUAD || TEAMS == 2, "a four-row box takes two teams");
   using T = typename PL::Scalar;
   using V = cplx<T>;
   using RT = RowTile<PL>;
@@ -866,20 +869,39 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
   }
   __syncthreads();
+  if constexpr (QUAD) {
+    V* stage = reinterpret_cast<V*>(smraw);
 #pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int kx = t + NT * i;
-    if (kx < HX) {
-      sm[2 * kx] = A[i];
-      sm[2 * kx + 1] = B[i];
+    for (int i = 0; i < NI; ++i) {
+      const int kx = t + NT * i;
+      if (kx < HX) {
+        stage[4 * kx + 2 * c] = A[i];
+        stage[4 * kx + 2 * c + 1] = B[i];
+      }
     }
-  }
-  fence_proxy_async();
-  __syncthreads();
-  if (t == 0 && active) {
-    for (int kx0 = 0; kx0 < HX; kx0 += RT::BOXK) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
-    tma_store_commit();
-    tma_store_wait_read();
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0 && 4 * (int)blockIdx.x < a.nrows) {
+      for (int kx0 = 0; kx0 < HX; kx0 += RT::BOXK) tma_store_3d(&omap, stage + 4 * kx0, 8 * blockIdx.x, kx0, s);
+      tma_store_commit();
+      tma_store_wait_read();
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int kx = t + NT * i;
+      if (kx < HX) {
+        sm[2 * kx] = A[i];
+        sm[2 * kx + 1] = B[i];
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (t == 0 && active) {
+      for (int kx0 = 0; kx0 < HX; kx0 += RT::BOXK) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
+      tma_store_commit();
+      tma_store_wait_read();
+    }
   }
 }
 
@@ -977,9 +999,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   if (t == 0) tma_store_wait_read();
 }
 
-template <class PL, int MAXT, int MINB, int TEAMS>
+template <class PL, int MAXT, int MINB, int TEAMS, bool QUAD = false>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
+  static_assert(!QUAD || TEAMS == 2, "a four-row box takes two teams");
   using T = typename PL::Scalar;
   using V = cplx<T>;
   using RT = RowTile<PL>;
@@ -991,22 +1014,43 @@ __global__ void __launch_bounds__(MAXT, MINB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots) + c;
   const int t = threadIdx.x - c * NT, s = blockIdx.y, ja = 2 * (blockIdx.x * TEAMS + c), jb = ja + 1;
   const bool active = ja < a.nrows;
-  if (t == 0 && active) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    // every box delivers its full extent (out-of-range rows zero-filled)
-    mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * RT::BOXK * 2 * sizeof(V)));
-    for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
-  }
-  __syncthreads();
-  if (active) mbar_wait(bar, 0);
   V A[NI], B[NI];
+  if constexpr (QUAD) {
+    V* stage = reinterpret_cast<V*>(smraw);
+    uint64_t* bar0 = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots);
+    if (threadIdx.x == 0) {
+      mbar_init(bar0, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar0, (uint32_t)(NBOX * RT::BOXK * 4 * sizeof(V)));
+      for (int b = 0; b < NBOX; ++b) tma_load_3d(stage + 4 * b * RT::BOXK, &imap, 8 * blockIdx.x, b * RT::BOXK, s, bar0);
+    }
+    __syncthreads();
+    mbar_wait(bar0, 0);
 #pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int kx = t + NT * i;
-    if (kx < HX) {
-      A[i] = sm[2 * kx];  // out-of-range rows arrive zero-filled
-      B[i] = sm[2 * kx + 1];
+    for (int i = 0; i < NI; ++i) {
+      const int kx = t + NT * i;
+      if (kx < HX) {
+        A[i] = stage[4 * kx + 2 * c];  // out-of-range rows arrive zero-filled
+        B[i] = stage[4 * kx + 2 * c + 1];
+      }
+    }
+  } else {
+    if (t == 0 && active) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      // every box delivers its full extent (out-of-range rows zero-filled)
+      mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * RT::BOXK * 2 * sizeof(V)));
+      for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
+    }
+    __syncthreads();
+    if (active) mbar_wait(bar, 0);
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int kx = t + NT * i;
+      if (kx < HX) {
+        A[i] = sm[2 * kx];  // out-of-range rows arrive zero-filled
+        B[i] = sm[2 * kx + 1];
+      }
     }
   }
   __syncthreads();
@@ -1186,7 +1230,22 @@ template <class PL> struct Shape {
   static constexpr int rowtma_minb = PL::kStatic ? minb(NT, 128) : 1;
   static constexpr int t2d_teams = T2D_TEAMS;
   static constexpr int t2d_minb = PL::kStatic ? minb(T2D_TEAMS * NT, row_regs) : 1;
+  static constexpr int quad_minb = PL::kStatic ? minb(2 * NT, row_regs) : 1;
 };
+
+bool env_flag(const char* name, bool dflt);
+
+// fp32 row passes move four rows per CTA (32-byte box rows); BTTB_QUAD=0 off
+// (fp64: opt-in BTTB_QUAD64=1, its box rows are already full sectors)
+template <class T> bool quad_rows() {
+  if constexpr (sizeof(T) == 4) {
+    static const bool on = !(getenv("BTTB_QUAD") && atoi(getenv("BTTB_QUAD")) == 0);
+    return on;
+  } else {
+    static const bool on = env_flag("BTTB_QUAD64", false);
+    return on;
+  }
+}
 
 bool tma_ok() {
   static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
@@ -1305,12 +1364,12 @@ bool t2d_ok() {
 // slabs), box (4 reals = 2 rows, 256 kx, 1 slab).
 template <class T>
 bool encode_rowpair_map(CUtensorMap* m, const void* base, int rows, int Hx, int slabs, long long ld_kx,
-                        long long ld_slab) {
+                        long long ld_slab, int box_rows = 2) {
   const size_t esz = sizeof(T);
   if (!al16(base) || (ld_kx * 2 * esz) % 16 || (ld_slab * 2 * esz) % 16) return false;
   cuuint64_t dims[3] = {(cuuint64_t)2 * rows, (cuuint64_t)Hx, (cuuint64_t)slabs};
   cuuint64_t strides[2] = {(cuuint64_t)(ld_kx * 2 * esz), (cuuint64_t)(ld_slab * 2 * esz)};
-  cuuint32_t box[3] = {4, (cuuint32_t)(Hx < kBoxKx ? Hx : kBoxKx), 1};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * box_rows), (cuuint32_t)(Hx < kBoxKx ? Hx : kBoxKx), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1372,6 +1431,16 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
         return cudaGetLastError();
       }
       CUtensorMap omap;
+      if (t2d_ok() && quad_rows<T>() && a.Hx <= 65535 &&
+          encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride, 4)) {
+        auto kern = k_row_r2c_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
+        const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd((a.nrows + 3) / 4, a.nslabs);
+        kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, omap);
+        return cudaGetLastError();
+      }
       if (t2d_ok() && a.Hx <= 65535 &&
           encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride)) {
         const size_t esz = sizeof(T);
@@ -1427,6 +1496,16 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
         return cudaGetLastError();
       }
       CUtensorMap imap;
+      if (t2d_ok() && quad_rows<T>() && !a.rowmajor &&
+          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 4)) {
+        auto kern = k_row_c2r_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
+        const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd((a.nrows + 3) / 4, a.nslabs);
+        kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
+        return cudaGetLastError();
+      }
       if (t2d_ok() && !a.rowmajor &&
           encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride)) {
         constexpr int TM = Shape<PL>::t2d_teams;
