@@ -289,11 +289,43 @@ __device__ __forceinline__ void team_fft(cplx<T> (&v)[E], cplx<T>* sm, int t, co
 // PP (per-pass twiddles): tw points at this pass's table, entry (r-1)*NS + k =
 // exp(-2*pi*i*r*k/(NS*R)) -- a warp's loads for one r are then contiguous in k
 // instead of striding r*k*L/(NS*R) through the length-L table.
+// exactly-rounded constant tables exist for these roots (twiddle_consts.h;
+// 1, 2, 4: quarter turns are exact)
+constexpr bool has_twr(int q) {
+  return q == 1 || q == 2 || q == 4 || q == 3 || q == 5 || q == 6 || q == 8 || q == 10 || q == 12 || q == 16 ||
+         q == 20 || q == 25;
+}
+
 template <class T, int E, int R, int NS, int NT, int L, bool PP = false>
 __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw) {
   using V = cplx<T>;
   constexpr int NB = E / R;
   constexpr int STRIDE = L / (NS * R);
+  // When a thread's blocks b sit at k = t + NT*b (NT*NB <= NS), the twiddle
+  // w^(r*k) of block b is block 0's times the constant w_Q^(r*b), Q = NS*R/NT:
+  // one table load per r instead of NB (the table loads are L1 wavefronts,
+  // the binding resource of the exchanges; the constant multiply is FP64 work).
+  constexpr bool DERIVE = PP && NS > 1 && NB > 1 && NT * NB <= NS && (NS * R) % NT == 0 && has_twr((NS * R) / NT);
+  if constexpr (DERIVE) {
+    constexpr int Q = (NS * R) / NT;
+    V w0[R];
+    sfor<1, R>([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      w0[r] = __ldg(&tw[(r - 1) * NS + t]);
+    });
+    sfor<0, NB>([&](auto bc) {
+      constexpr int b = decltype(bc)::value;
+      V u[R];
+      sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; u[r] = v[b + r * NB]; });
+      sfor<1, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        u[r] = cmul(u[r], b == 0 ? w0[r] : twc<Q, (r * b) % Q>(w0[r]));
+      });
+      dft<R>(u);
+      sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; v[b + r * NB] = u[r]; });
+    });
+    return;
+  }
   sfor<0, NB>([&](auto bc) {
     constexpr int b = decltype(bc)::value;
     V u[R];
