@@ -89,6 +89,19 @@ int bttb_plan_destroy(bttb_plan* plan);
  * (host memory; copies in and out, synchronous). */
 int bttb_apply(bttb_plan* plan, int mode, const void* x, void* y, int64_t batch, int where, void* stream);
 
+/* Device-resident batched CGLS -- the inversion loop the paper names as future
+ * work (no reference function: the reference stops at apply,
+ * multiply.py:22-58, and lists inversion as a non-goal).
+ * Minimises |G m - d|^2 + damp^2 |m|^2 from m = 0 for `batch` independent
+ * data vectors with `iters` CGLS iterations (one forward and one transpose
+ * product each, fused vector updates, fp64 reductions, no host round trip
+ * inside the loop).  d = batch x m, m_out = batch x n (the plan must hold every
+ * layer).  where / stream as in bttb_apply.  resid_norms (optional host
+ * array, batch x (iters+1)) receives |d - G m_k| for k = 0..iters; the call
+ * then synchronises. */
+int bttb_cgls(bttb_plan* plan, const void* d, void* m_out, int64_t batch, int iters, double damp, int where,
+              void* stream, double* resid_norms);
+
 /* Entry-generator parity hook: the layer's response window, shape
  * (sx+nx-1) x (sy+ny-1), row-major, as layer_response_window returns it
  * (kernels.py:158-184).  `layer` is a global layer index. */

@@ -22,7 +22,7 @@ __all__ = [
     "mag_constants", "gravity_corner_sum", "magnetic_entries",
     "layer_window", "embed_window", "transpose_defining_array",
     "build_spectra", "forward", "transpose", "rel_l2", "make_inputs",
-    "blob_model", "CONFIGS", "config_grid", "config_kernel",
+    "blob_model", "CONFIGS", "config_grid", "config_kernel", "cgls",
 ]
 
 #: CODATA gravitational constant (``kernels.py:16``).
@@ -279,6 +279,37 @@ def rel_l2(a, b):
     if na == 0.0:
         return 0.0 if nd == 0.0 else np.inf
     return nd / na
+
+
+def cgls(g, fw, tr, d, iters, damp=0.0, rtol=1e-13):
+    """Textbook CGLS on min |G m - d|^2 + damp^2 |m|^2 from m = 0 (the checker
+    of ``bttb_cgls``; the reference has no inversion loop -- PAPER.md:640 names
+    it future work, SPEC.md:320 a non-goal -- so this restates the standard
+    algorithm over the pinned ``forward``/``transpose`` above).  Like the
+    device loop it freezes (alpha = beta = 0) once |s_k| <= rtol |s_0|: past
+    convergence CG only amplifies rounding noise.  Returns
+    (m, [|r_0|, ..., |r_iters|])."""
+    d = np.asarray(d, dtype=float)
+    m = np.zeros(len(tr) * g.n_r)
+    r = d.copy()
+    s = transpose(g, tr, r)
+    p = s.copy()
+    gamma = float(s @ s)
+    floor = rtol * rtol * gamma
+    hist = [float(np.linalg.norm(r))]
+    for _ in range(iters):
+        q = forward(g, fw, p)
+        delta = float(q @ q) + damp * damp * float(p @ p)
+        alpha = gamma / delta if (delta > 0 and gamma > floor) else 0.0
+        m = m + alpha * p
+        r = r - alpha * q
+        s = transpose(g, tr, r) - damp * damp * m
+        gnew = float(s @ s)
+        beta = gnew / gamma if gamma > floor else 0.0
+        gamma = gnew
+        p = s + beta * p
+        hist.append(float(np.linalg.norm(r)))
+    return m, hist
 
 
 # --------------------------------------------------------------------------

@@ -22,6 +22,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", CSRC, "
 UNITS = {
     "entries.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"],
     "spectral.cu": ["-Xptxas", "-v"] if os.environ.get("BTTB_PTXAS_VERBOSE") else [],
+    "cgls.cu": [],
     "capi.cu": [],
 }
 

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "bttb_sm100.h"
+#include "cgls.h"
 #include "entries.h"
 #include "spectral.h"
 
@@ -277,6 +278,7 @@ struct bttb_plan_s {
   size_t elem = 16;
   void* spectra = nullptr;
   DevBuf work, hin, hout;
+  DevBuf cg;  // CGLS driver workspace (bttb_cgls)
   cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
   cudaStream_t stream2 = nullptr;  // second stream: column stages, overlapped with the next chunk's row pass
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -819,6 +821,7 @@ void destroy_plan(bttb_plan_s* p) {
   p->fx.release();
   p->fy.release();
   p->work.release();
+  p->cg.release();
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->stream2) cudaStreamDestroy(p->stream2);
   for (int i = 0; i < 2; ++i) {
@@ -831,6 +834,67 @@ void destroy_plan(bttb_plan_s* p) {
   p->hin.release();
   p->hout.release();
   delete p;
+}
+
+}  // namespace
+
+namespace {
+
+// Device-resident batched CGLS (PAPER.md:640 future work).
+// Textbook CGLS (Hestenes-Stiefel form on the normal equations) from m0 = 0:
+//   r = d, s = G^T r, p = s, gamma = |s|^2
+//   per iteration: q = G p; alpha = gamma / (|q|^2 + damp^2 |p|^2);
+//                  m += alpha p; r -= alpha q; s = G^T r - damp^2 m;
+//                  beta = |s|^2 / gamma; gamma = |s|^2; p = s + beta p.
+// Everything stays on the plan's stream: products through run_apply, vector
+// updates and fp64 reductions through cgls.cu, scalars in device memory.
+// Converged items freeze (alpha = beta = 0) once |s_k| <= rtol |s_0|, rtol =
+// 1e-13 (fp64) / 1e-6 (fp32): past convergence CG only amplifies rounding.
+template <class T>
+int run_cgls(bttb_plan_s* p, const T* d, T* mo, int64_t batch, int iters, double damp, double* hist_dev,
+                    cudaStream_t st) {
+  const int64_t m = p->m(), n = p->nloc();
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+  const int bm = cgls_blocks(m, (int)batch, nsm), bn = cgls_blocks(n, (int)batch, nsm);
+  const double damp2 = damp * damp;
+  const size_t vm = round_up(sizeof(T) * m * batch, 256), vn = round_up(sizeof(T) * n * batch, 256);
+  const size_t pa = round_up(sizeof(double) * batch * (bm > bn ? bm : bn), 256);
+  const size_t scb = round_up(sizeof(CglsScalars) * batch, 256);
+  int rc;
+  if ((rc = p->cg.ensure(2 * vm + 2 * vn + 2 * pa + scb))) return rc;
+  char* w = static_cast<char*>(p->cg.p);
+  T* r = reinterpret_cast<T*>(w);
+  T* q = reinterpret_cast<T*>(w + vm);
+  T* s = reinterpret_cast<T*>(w + 2 * vm);
+  T* pv = reinterpret_cast<T*>(w + 2 * vm + vn);
+  double* pa0 = reinterpret_cast<double*>(w + 2 * vm + 2 * vn);
+  double* pa1 = reinterpret_cast<double*>(w + 2 * vm + 2 * vn + pa);
+  CglsScalars* sc = reinterpret_cast<CglsScalars*>(w + 2 * vm + 2 * vn + 2 * pa);
+  const int hld = iters + 1;
+  CU(cudaMemcpyAsync(r, d, sizeof(T) * m * batch, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemsetAsync(mo, 0, sizeof(T) * n * batch, st));
+  if ((rc = run_apply<T>(p, BTTB_TRANSPOSE, r, s, batch, st))) return rc;
+  CU(cgls_dot<T>(s, s, n, (int)batch, bn, pa0, st));
+  CU(cgls_dot<T>(r, r, m, (int)batch, bm, pa1, st));
+  CU(cgls_scalars(CGLS_INIT, (int)batch, pa0, bn, pa1, bm, damp2, sizeof(T) == 8 ? 1e-13 : 1e-6, sc, hist_dev, hld, 0,
+                    st));
+  CU(cudaMemcpyAsync(pv, s, sizeof(T) * n * batch, cudaMemcpyDeviceToDevice, st));
+  for (int it = 0; it < iters; ++it) {
+    if ((rc = run_apply<T>(p, BTTB_FORWARD, pv, q, batch, st))) return rc;
+    CU(cgls_dot<T>(q, q, m, (int)batch, bm, pa0, st));
+    if (damp2 != 0.0) CU(cgls_dot<T>(pv, pv, n, (int)batch, bn, pa1, st));
+    CU(cgls_scalars(CGLS_ALPHA, (int)batch, pa0, bm, damp2 != 0.0 ? pa1 : nullptr, bn, damp2, 0.0, sc, nullptr, hld,
+                    0, st));
+    CU(cgls_resid<T>(r, q, m, (int)batch, bm, sc, pa1, st));
+    if ((rc = run_apply<T>(p, BTTB_TRANSPOSE, r, s, batch, st))) return rc;
+    // |s|^2 partials; damped: first m += alpha p and s -= damp^2 m
+    CU(cgls_update<T>(mo, pv, s, n, (int)batch, bn, sc, damp2, pa0, 0, st));
+    CU(cgls_scalars(CGLS_BETA, (int)batch, pa0, bn, pa1, bm, damp2, 0.0, sc, hist_dev, hld, it + 1, st));
+    CU(cgls_update<T>(mo, pv, s, n, (int)batch, bn, sc, damp2, nullptr, 1, st));
+  }
+  p->last_launches = 0;
+  return BTTB_OK;
 }
 
 }  // namespace
@@ -1003,6 +1067,53 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
     CU(cudaStreamSynchronize(st));
     if (p->pipe_err_host && *p->pipe_err_host) return fail(BTTB_ECUDA, "fused pipeline deadlock guard tripped");
   }
+  return BTTB_OK;
+}
+
+int bttb_cgls(bttb_plan* p, const void* d, void* m_out, int64_t batch, int iters, double damp, int where,
+              void* stream, double* resid_norms) {
+  g_err.clear();
+  if (!p || !d || !m_out) return fail(BTTB_EINVAL, "null argument");
+  if (batch < 0 || iters < 0) return fail(BTTB_EINVAL, "batch and iters must be >= 0");
+  if (!(damp >= 0.0) || !std::isfinite(damp)) return fail(BTTB_EINVAL, "damp must be finite and >= 0");
+  if (p->l0 != 0 || p->l1 != p->nz)
+    return fail(BTTB_EINVAL, "cgls needs a plan holding every layer (this plan holds [%lld, %lld) of %lld)",
+                (long long)p->l0, (long long)p->l1, (long long)p->nz);
+  if (where != BTTB_DEVICE_PTR && where != BTTB_HOST_PTR)
+    return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR or BTTB_HOST_PTR");
+  if (batch == 0) return BTTB_OK;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t esz = p->elem / 2;
+  const size_t dbytes = (size_t)batch * p->m() * esz, mbytes = (size_t)batch * p->nloc() * esz;
+  const void* dd = d;
+  void* md = m_out;
+  int rc;
+  if (where == BTTB_HOST_PTR) {
+    if ((rc = p->hin.ensure(dbytes)) || (rc = p->hout.ensure(mbytes))) return rc;
+    CU(cudaMemcpyAsync(p->hin.p, d, dbytes, cudaMemcpyHostToDevice, st));
+    dd = p->hin.p;
+    md = p->hout.p;
+  }
+  double* hist = nullptr;
+  if (resid_norms) CU(cudaMallocAsync(reinterpret_cast<void**>(&hist), sizeof(double) * batch * (iters + 1), st));
+  CU(cudaEventRecord(p->ev_in, st));
+  CU(cudaStreamWaitEvent(p->stream, p->ev_in, 0));
+  rc = p->dtype == BTTB_F64
+           ? run_cgls<double>(p, static_cast<const double*>(dd), static_cast<double*>(md), batch, iters, damp, hist,
+                              p->stream)
+           : run_cgls<float>(p, static_cast<const float*>(dd), static_cast<float*>(md), batch, iters, damp, hist,
+                             p->stream);
+  if (rc) return rc;
+  CU(cudaEventRecord(p->ev_out, p->stream));
+  CU(cudaStreamWaitEvent(st, p->ev_out, 0));
+  if (where == BTTB_HOST_PTR) CU(cudaMemcpyAsync(m_out, md, mbytes, cudaMemcpyDeviceToHost, st));
+  if (resid_norms) {
+    CU(cudaMemcpyAsync(resid_norms, hist, sizeof(double) * batch * (iters + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaFreeAsync(hist, st));
+  }
+  if (where == BTTB_HOST_PTR || resid_norms) CU(cudaStreamSynchronize(st));
   return BTTB_OK;
 }
 

@@ -296,11 +296,47 @@ constexpr bool has_twr(int q) {
          q == 20 || q == 25;
 }
 
+// Generated pass twiddles (BTTB_TWGEN, default on): of the R-1 twiddles
+// w^(r*k) of a butterfly only w^k and w^(Q*k) (Q ~ sqrt(R)) are loaded from
+// the per-pass table; the rest are products w^(a*Q*k) * w^(c*k) of powers of
+// the two (at most ~5 roundings: relative error < 1e-15 in fp64).  A table
+// load is a 512-byte warp access of the L1 data pipe that binds the FFT
+// passes (4 wavefronts), a complex multiply is 4 FP64 (or FP32) instructions
+// on a pipe with headroom.
+#ifndef BTTB_TWGEN
+#define BTTB_TWGEN 1
+#endif
+template <int R> struct TwQ {
+  static constexpr int Q = R >= 16 ? 4 : R >= 8 ? 4 : R >= 4 ? 2 : 1;
+};
+template <class V, int R, int NS>
+__device__ __forceinline__ void gen_twiddles(V (&w)[R], const V* __restrict__ tw, int k) {
+  constexpr int Q = TwQ<R>::Q;
+  w[1] = __ldg(&tw[k]);
+  if constexpr (Q > 1 && Q < R) w[Q] = __ldg(&tw[(Q - 1) * NS + k]);
+  sfor<2, (Q < R ? Q : R)>([&](auto cc) {
+    constexpr int c = decltype(cc)::value;
+    w[c] = cmul(w[c - 1], w[1]);
+  });
+  sfor<2, (R + Q - 1) / Q>([&](auto ac) {
+    constexpr int a = decltype(ac)::value;
+    w[a * Q] = cmul(w[(a - 1) * Q], w[Q]);
+  });
+  sfor<1, (R + Q - 1) / Q>([&](auto ac) {
+    constexpr int a = decltype(ac)::value;
+    sfor<1, Q>([&](auto cc) {
+      constexpr int c = decltype(cc)::value;
+      if constexpr (a * Q + c < R) w[a * Q + c] = cmul(w[a * Q], w[c]);
+    });
+  });
+}
+
 template <class T, int E, int R, int NS, int NT, int L, bool PP = false>
 __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw) {
   using V = cplx<T>;
   constexpr int NB = E / R;
   constexpr int STRIDE = L / (NS * R);
+  constexpr bool GEN = BTTB_TWGEN && PP && NS > 1 && R >= 4;
   // When a thread's blocks b sit at k = t + NT*b (NT*NB <= NS), the twiddle
   // w^(r*k) of block b is block 0's times the constant w_Q^(r*b), Q = NS*R/NT:
   // one table load per r instead of NB (the table loads are L1 wavefronts,
@@ -309,10 +345,14 @@ __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx
   if constexpr (DERIVE) {
     constexpr int Q = (NS * R) / NT;
     V w0[R];
-    sfor<1, R>([&](auto rc) {
-      constexpr int r = decltype(rc)::value;
-      w0[r] = __ldg(&tw[(r - 1) * NS + t]);
-    });
+    if constexpr (GEN) {
+      gen_twiddles<V, R, NS>(w0, tw, t);
+    } else {
+      sfor<1, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        w0[r] = __ldg(&tw[(r - 1) * NS + t]);
+      });
+    }
     sfor<0, NB>([&](auto bc) {
       constexpr int b = decltype(bc)::value;
       V u[R];
@@ -330,7 +370,15 @@ __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx
     constexpr int b = decltype(bc)::value;
     V u[R];
     sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; u[r] = v[b + r * NB]; });
-    if constexpr (NS > 1) {
+    if constexpr (GEN) {
+      const int k = (t + NT * b) % NS;
+      V w[R];
+      gen_twiddles<V, R, NS>(w, tw, k);
+      sfor<1, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        u[r] = cmul(u[r], w[r]);
+      });
+    } else if constexpr (NS > 1) {
       const int k = (t + NT * b) % NS;
       sfor<1, R>([&](auto rc) {
         constexpr int r = decltype(rc)::value;
