@@ -42,6 +42,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cgls", type=int, default=0, metavar="ITERS",
+                    help="time the device-resident batched CGLS driver instead: one step = ITERS "
+                         "iterations (one G*m and one G^T*d each) over the config's batch; under "
+                         "torchrun the batch's models are sharded over the ranks")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints nothing")
@@ -428,10 +432,150 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# CGLS arm (--cgls ITERS): SURVEY.md 8(f)3, BASELINE config C5
+# ---------------------------------------------------------------------------
+def cgls_cpu_sample(cfg, iters):
+    """The oracle's CGLS (numpy, 1 thread) on ONE model of the config's geometry."""
+    from oracle import bttb_oracle as O
+
+    g = O.config_grid(cfg)
+    kind, consts = O.config_kernel(cfg)
+    fw, tr = O.build_spectra(g, kind, consts)
+    d = np.random.default_rng(1).normal(0.0, 1.0, g.m)
+    it = max(1, min(iters, 3))
+    t0 = time.perf_counter()
+    O.cgls(g, fw, tr, d, it)
+    dt = time.perf_counter() - t0
+    return {"value": g.n * it / dt, "unit": "voxels/s", "cores": 1, "kind": "port",
+            "sample": f"{cfg} geometry, 1 model, {it} CGLS iterations of the oracle (numpy pocketfft, "
+                      f"reference algorithm per product), {dt:.2f} s"}
+
+
+def run_cgls(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_06976_b200 as B
+    from oracle import bttb_oracle as O  # input recipe + cpu baseline only
+
+    rank, world, local = dist_env()
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, iters = a.config, a.cgls
+    desc, batch = workload(cfg, O)
+    og = O.config_grid(cfg)
+    kind, _ = O.config_kernel(cfg)
+    sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, dz, _, kargs, _ = O.CONFIGS[cfg]
+    grid = B.make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, og.z)
+    params = B.KernelParams.gravity() if kind == "gravity" else B.KernelParams.magnetic(*kargs)
+    # models sharded over ranks (replicas of the whole stack, no collective in the loop)
+    b0, b1 = batch * rank // world, batch * (rank + 1) // world
+    nb = b1 - b0
+    np_dt = np.float64 if a.dtype == "f64" else np.float32
+    bsz = 8 if a.dtype == "f64" else 4
+    t0 = time.perf_counter()
+    stack = B.build_transform_stack(grid, params, dtype="float64" if a.dtype == "f64" else "float32",
+                                    device=local)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    # data of the batch: G applied to seeded N(0, 0.1) models (the C5 recipe) plus noise
+    rng = np.random.default_rng(1000)
+    truth = rng.normal(0.0, 0.1, (batch, grid.n))[b0:b1]
+    dgen = B.apply(stack, torch.tensor(truth, device=dev), "forward")
+    dgen += 1e-3 * dgen.abs().max() * torch.randn(dgen.shape, generator=torch.Generator(device=dev).manual_seed(7),
+                                                   device=dev, dtype=dgen.dtype)
+    d_dev = dgen.contiguous()
+    d_pin = d_dev.cpu().pin_memory()
+
+    def step():
+        return B.cgls(stack, d_dev, iters=iters, history=False)[0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    # one product of each kind for the launch count and the roofline split
+    m_dev = step()
+    _, hist = B.cgls(stack, d_dev, iters=iters)
+    launches = int(stack.info()[9])
+    # end to end: host data in, host models out, through the public API (numpy -> C ABI host path)
+    d_host = d_pin.numpy()
+    B.cgls(stack, d_host, iters=iters, history=False)
+    barrier()
+    t0 = time.perf_counter()
+    e_steps = max(2, min(a.steps, 5))
+    for _ in range(e_steps):
+        B.cgls(stack, d_host, iters=iters, history=False)
+    barrier()
+    t_e2e = (time.perf_counter() - t0) / e_steps
+    vals = torch.tensor([ms, t_e2e], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, t_e2e = vals.tolist()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    peak, peak_kind = peaks()
+    B_apply = algorithmic_bytes(og, bsz, batch)
+    # per iteration: one forward + one transpose (+ one transpose to start)
+    napply = 2 * iters + 1
+    achieved = napply * B_apply / (ms * 1e-3) / 1e9
+    cpu = None if (a.no_cpu_baseline or world > 1) else cgls_cpu_sample(cfg, iters)
+    rel_drop = float(np.median(hist[:, -1] / hist[:, 0]))
+    line = {
+        "metric": METRIC, "value": batch * grid.n * iters / (ms * 1e-3), "unit": "voxels/s",
+        "n_gpus": world, "steps": a.steps, "warmup": max(3, a.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": a.dtype,
+        "data": "synthetic: seeded N(0,0.1) models through the operator plus 0.1% noise, resident in HBM",
+        "config": {"workload": desc, "step": f"{iters} CGLS iterations (G*m + G^T*d each) over the batch",
+                   "fft_shape": list(stack.fft_shape), "models_per_rank": nb,
+                   "parallelism": f"model-shard x{world} (replicated stack)",
+                   "l2": "per-iteration vectors (%.2f GB) larger than L2" % (3 * nb * grid.n * bsz / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                     "algorithmic_bytes_per_apply": B_apply,
+                     "kernel": "CGLS loop: fused operator products + fused vector updates"},
+        "build_s": t_build, "residual_drop_median": rel_drop,
+        "cpu_baseline": cpu,
+        "e2e": {"value": batch * grid.n * iters / t_e2e, "unit": "voxels/s",
+                "h2d_bytes_per_step": int(d_host.size * bsz), "d2h_bytes_per_step": int(nb * grid.n * bsz),
+                "ms_per_step": 1e3 * t_e2e},
+        "clocks": clocks,
+        "gpu_launches": launches * a.steps, "launches_per_step": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.cgls > 0:
+        run_cgls(a)
     else:
         run_ours(a)
 

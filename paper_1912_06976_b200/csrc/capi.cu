@@ -872,9 +872,11 @@ int run_cgls(bttb_plan_s* p, const T* d, T* mo, int64_t batch, int iters, double
   double* pa1 = reinterpret_cast<double*>(w + 2 * vm + 2 * vn + pa);
   CglsScalars* sc = reinterpret_cast<CglsScalars*>(w + 2 * vm + 2 * vn + 2 * pa);
   const int hld = iters + 1;
+  int64_t nl = 0;  // kernels launched (operator products + vector kernels)
   CU(cudaMemcpyAsync(r, d, sizeof(T) * m * batch, cudaMemcpyDeviceToDevice, st));
   CU(cudaMemsetAsync(mo, 0, sizeof(T) * n * batch, st));
   if ((rc = run_apply<T>(p, BTTB_TRANSPOSE, r, s, batch, st))) return rc;
+  nl += p->last_launches + 3;
   CU(cgls_dot<T>(s, s, n, (int)batch, bn, pa0, st));
   CU(cgls_dot<T>(r, r, m, (int)batch, bm, pa1, st));
   CU(cgls_scalars(CGLS_INIT, (int)batch, pa0, bn, pa1, bm, damp2, sizeof(T) == 8 ? 1e-13 : 1e-6, sc, hist_dev, hld, 0,
@@ -882,18 +884,20 @@ int run_cgls(bttb_plan_s* p, const T* d, T* mo, int64_t batch, int iters, double
   CU(cudaMemcpyAsync(pv, s, sizeof(T) * n * batch, cudaMemcpyDeviceToDevice, st));
   for (int it = 0; it < iters; ++it) {
     if ((rc = run_apply<T>(p, BTTB_FORWARD, pv, q, batch, st))) return rc;
+    nl += p->last_launches + (damp2 != 0.0 ? 7 : 6);
     CU(cgls_dot<T>(q, q, m, (int)batch, bm, pa0, st));
     if (damp2 != 0.0) CU(cgls_dot<T>(pv, pv, n, (int)batch, bn, pa1, st));
     CU(cgls_scalars(CGLS_ALPHA, (int)batch, pa0, bm, damp2 != 0.0 ? pa1 : nullptr, bn, damp2, 0.0, sc, nullptr, hld,
                     0, st));
     CU(cgls_resid<T>(r, q, m, (int)batch, bm, sc, pa1, st));
     if ((rc = run_apply<T>(p, BTTB_TRANSPOSE, r, s, batch, st))) return rc;
+    nl += p->last_launches;
     // |s|^2 partials; damped: first m += alpha p and s -= damp^2 m
     CU(cgls_update<T>(mo, pv, s, n, (int)batch, bn, sc, damp2, pa0, 0, st));
     CU(cgls_scalars(CGLS_BETA, (int)batch, pa0, bn, pa1, bm, damp2, 0.0, sc, hist_dev, hld, it + 1, st));
     CU(cgls_update<T>(mo, pv, s, n, (int)batch, bn, sc, damp2, nullptr, 1, st));
   }
-  p->last_launches = 0;
+  p->last_launches = nl;
   return BTTB_OK;
 }
 

@@ -29,8 +29,14 @@
 #ifndef ROW_REGS_F32
 #define ROW_REGS_F32 128  // register target of the fp32 row passes (80, 96 measured slower)
 #endif
+#ifndef ROW_REGS_F64
+#define ROW_REGS_F64 128  // register target of the fp64 row passes
+#endif
 #ifndef COL_REGS_F32
 #define COL_REGS_F32 168  // register target of the fp32 column stages (96, 128 measured slower)
+#endif
+#ifndef TRA_REGS_F64
+#define TRA_REGS_F64 168  // register target of the fp64 TMA transpose column stage (see Shape::tra_regs)
 #endif
 #ifndef T2D_TEAMS
 #define T2D_TEAMS 1  // row pairs (teams) per CTA of the tensor-TMA row passes
@@ -856,28 +862,31 @@ __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
   for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
   __syncthreads();
+  // Separation, one stage element per lane: element e of the team's [kx][2]
+  // tile is A (e even) or B (e odd) of kx = e/2, so a warp's tile stores are
+  // contiguous 16-byte lanes (the [kx] x {A, B} pairs at a 32-byte stride cost
+  // twice the shared-memory wavefronts); the two lanes of a kx read the same
+  // zk / zm (broadcast).
   const T h = T(0.5);
-  V A[NI], B[NI];
+  constexpr int NE = (2 * HX + NT - 1) / NT;
+  V P[NE];
 #pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int kx = t + NT * i;
+  for (int i = 0; i < NE; ++i) {
+    const int e = t + NT * i, kx = e >> 1;
     if (kx < HX) {
       const V zk = sm[PL::slot(kx)];
       const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
-      A[i] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
-      B[i] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+      const bool odd = e & 1;
+      P[i] = mkc<V>(h * (odd ? zk.y + zm.y : zk.x + zm.x), h * (odd ? zm.x - zk.x : zk.y - zm.y));
     }
   }
   __syncthreads();
   if constexpr (QUAD) {
     V* stage = reinterpret_cast<V*>(smraw);
 #pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const int kx = t + NT * i;
-      if (kx < HX) {
-        stage[4 * kx + 2 * c] = A[i];
-        stage[4 * kx + 2 * c + 1] = B[i];
-      }
+    for (int i = 0; i < NE; ++i) {
+      const int e = t + NT * i;
+      if (e < 2 * HX) stage[4 * (e >> 1) + 2 * c + (e & 1)] = P[i];
     }
     fence_proxy_async();
     __syncthreads();
@@ -888,12 +897,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const int kx = t + NT * i;
-      if (kx < HX) {
-        sm[2 * kx] = A[i];
-        sm[2 * kx + 1] = B[i];
-      }
+    for (int i = 0; i < NE; ++i) {
+      const int e = t + NT * i;
+      if (e < 2 * HX) sm[e] = P[i];
     }
     fence_proxy_async();
     __syncthreads();
@@ -1219,7 +1225,7 @@ template <class PL> struct Shape {
   static constexpr int col_regs_rounded =
       col_regs <= 96 ? 96 : col_regs <= 128 ? 128 : (col_regs <= 144 ? 144 : (col_regs <= 168 ? 168 : 255));
   // row passes hold E complex values plus the separated tile: fp32 needs far fewer registers
-  static constexpr int row_regs = sizeof(T) == 8 ? 128 : ROW_REGS_F32;
+  static constexpr int row_regs = sizeof(T) == 8 ? ROW_REGS_F64 : ROW_REGS_F32;
   static constexpr int row_minb = PL::kStatic ? minb(row_threads, 128) : 1;
   // fp64 plans with 20 elements per thread keep the column accumulator in
   // shared memory (registers would cap occupancy at two teams per SM)
@@ -1227,6 +1233,13 @@ template <class PL> struct Shape {
   static constexpr int col_minb = PL::kStatic ? minb(col_threads, acc_smem ? 168 : col_regs_rounded) : 1;
   static constexpr int spec_minb = PL::kStatic ? minb(col_threads, 128) : 1;
   static constexpr int tma_minb = PL::kStatic ? minb(col_threads, col_regs_rounded) : 1;
+  // the TMA transpose column stage stages only the spectrum (exchange + S: 67 KB
+  // at fp64 L=2048), so three CTAs fit an SM's shared memory if registers allow:
+  // fp64 plans of <= 16 elements run at TRA_REGS_F64 (C4 fp64: 1.95 -> 1.88 ms per
+  // transpose at 168; the forward also stages Y, 83 KB, and stays at two CTAs)
+  static constexpr int tra_regs =
+      (sizeof(T) == 8 && PL::E <= 16 && col_regs_rounded > TRA_REGS_F64) ? TRA_REGS_F64 : col_regs_rounded;
+  static constexpr int tra_minb = PL::kStatic ? minb(col_threads, tra_regs) : 1;
   static constexpr int rowtma_minb = PL::kStatic ? minb(NT, 128) : 1;
   static constexpr int t2d_teams = T2D_TEAMS;
   static constexpr int t2d_minb = PL::kStatic ? minb(T2D_TEAMS * NT, row_regs) : 1;
@@ -1601,7 +1614,7 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
     if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
-        auto kern = k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
+        auto kern = k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tra_minb>;
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;

@@ -35,7 +35,12 @@ def test_sizes_command(tmp_path):
     out = tmp_path / "sizes.csv"
     assert main(["sizes", "--padding", "0.05", "--out", str(out)]) == 0
     rows = out.read_text().strip().splitlines()
-    assert rows[0].startswith("problem,") and rows[1].endswith(",918") and len(rows) == 13
+    assert rows[0].startswith("problem,") and len(rows) == 13
+    hdr = rows[0].split(",")
+    first = dict(zip(hdr, rows[1].split(",")))
+    # the reference's columns (harness.py:55-64), then the GPU plan's FFT shape and cache bytes
+    assert hdr[:10] == ["problem", "sx", "sy", "nz", "pxl", "pyl", "nx", "ny", "m", "n"]
+    assert first["n"] == "918" and first["gpu_fft_shape"] == "64x32"
 
 
 def test_unknown_config_key_rejected(tmp_path, capsys):

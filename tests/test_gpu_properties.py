@@ -122,3 +122,17 @@ def test_spectrum_is_hermitian_consistent_and_cached():
         np.testing.assert_allclose(col[1:], np.conj(col[1:][::-1]), rtol=0, atol=1e-12 * np.abs(col).max())
         assert st.element_count == g.nz * g.embed_shape[0] * g.embed_shape[1]
         assert st.device_bytes == g.nz * (Lx // 2 + 1) * Ly * 16
+
+
+def test_cli_bench_writes_transform_gpu_rows(tmp_path):
+    import csv
+
+    from paper_1912_06976_b200 import cli
+
+    out = tmp_path / "bench.csv"
+    assert cli.main(["bench", "--problems", "1-2", "--trials", "2", "--padding", "0.1", "--out", str(out)]) == 0
+    rows = list(csv.DictReader(open(out)))
+    assert [(r["problem"], r["phase"]) for r in rows] == [
+        ("1", "build"), ("1", "forward"), ("1", "transpose"), ("2", "build"), ("2", "forward"), ("2", "transpose")]
+    assert all(r["path"] == "transform-gpu" and r["mean_rel_error_vs_dense"] == "" for r in rows)
+    assert all(float(r["mean_seconds"]) > 0 for r in rows)

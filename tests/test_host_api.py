@@ -138,3 +138,23 @@ def test_product_package_does_not_import_the_oracle():
             "[m for m in sys.modules if m.startswith('oracle')]")
     subprocess.run([sys.executable, "-c", code], check=True,
                    cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+
+
+def test_bench_csv_schema_matches_reference_columns():
+    # harness.py:20-43 of the reference: same columns, same float format, "" for None
+    from paper_1912_06976_b200.harness import CSV_COLUMNS, BenchRecord, bench_csv_text
+
+    assert CSV_COLUMNS == ("schema_version", "problem", "padding", "kernel", "path", "phase",
+                           "trials", "mean_seconds", "mean_rel_error_vs_dense", "m", "n", "seed")
+    rec = BenchRecord(problem=2, padding=0.1, kernel="gravity", path="transform-gpu", phase="forward",
+                      trials=5, mean_seconds=1.5e-3, mean_rel_error=None, m=1500, n=8640, seed=0)
+    lines = bench_csv_text([rec]).splitlines()
+    assert lines[0] == ",".join(CSV_COLUMNS)
+    assert lines[1] == "1,2,0.1,gravity,transform-gpu,forward,5,1.500000000e-03,,1500,8640,0"
+
+
+def test_cli_bench_rejects_bad_problem_index(capsys):
+    from paper_1912_06976_b200 import cli
+
+    assert cli.main(["bench", "--problems", "13"]) == 2
+    assert "unknown problem index 13" in capsys.readouterr().err

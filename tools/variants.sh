@@ -5,7 +5,7 @@
 mkdir -p gpurun_out/var
 for spec in "$@"; do
   label="${spec%%|*}"; envs="${spec#*|}"
-  env $envs timeout 300 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/var/$label.log 2>&1
+  env $envs timeout 300 python bench.py --steps ${STEPS:-30} --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/var/$label.log 2>&1
   python - "$label" << 'PY'
 import json, sys
 lab = sys.argv[1]
