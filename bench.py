@@ -503,6 +503,14 @@ def run_cgls(a):
     for _ in range(max(3, a.warmup)):
         step()
     barrier()
+    if a.profile_step:
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        if world > 1:
+            dist.destroy_process_group()
+        return
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.15)

@@ -16,6 +16,9 @@
 // scalars are fp64 for both.
 #include <cuda_runtime.h>
 
+#include <cstring>
+#include <type_traits>
+
 #include "cgls.h"
 
 namespace bttb {
@@ -40,15 +43,55 @@ __device__ __forceinline__ double block_sum(double v) {
   return s;  // valid in thread 0
 }
 
-// slice [lo, hi) of item blockIdx.y handled by block blockIdx.x
-struct Slice {
-  long long lo, hi;
+// 16-byte packs: the vector kernels stream with 128-bit accesses when an
+// item's length allows (every slice then starts on a pack boundary)
+template <class T> struct VecOf;
+template <> struct VecOf<float> { using type = float4; static constexpr int N = 4; };
+template <> struct VecOf<double> { using type = double2; static constexpr int N = 2; };
+
+template <class T, int N> struct Pack {
+  T v[N];
 };
-__device__ __forceinline__ Slice slice_of(long long len) {
-  const long long chunk = (len + gridDim.x - 1) / gridDim.x;
+template <class T, int N> __device__ __forceinline__ Pack<T, N> ld(const T* p) {
+  Pack<T, N> r;
+  if constexpr (N == 1) {
+    r.v[0] = *p;
+  } else {
+    using W = typename VecOf<T>::type;
+    const W w = *reinterpret_cast<const W*>(p);
+    static_assert(sizeof(W) == sizeof(Pack<T, N>), "pack size");
+    memcpy(&r, &w, sizeof(W));
+  }
+  return r;
+}
+template <class T, int N> __device__ __forceinline__ void st(T* p, const Pack<T, N>& r) {
+  if constexpr (N == 1) {
+    *p = r.v[0];
+  } else {
+    using W = typename VecOf<T>::type;
+    W w;
+    memcpy(&w, &r, sizeof(W));
+    *reinterpret_cast<W*>(p) = w;
+  }
+}
+
+// Block blockIdx.x's slice of item blockIdx.y: body(i, N) on elements
+// [i, i+N) of the item, N = the pack width when len is a multiple of it (the
+// slice bounds then are too), else 1.
+template <class T, class F> __device__ __forceinline__ void for_slice(long long len, F&& body) {
+  constexpr int VN = VecOf<T>::N;
+  const bool vec = len % VN == 0;
+  long long chunk = (len + gridDim.x - 1) / gridDim.x;
+  chunk = (chunk + VN - 1) / VN * VN;
   const long long lo = chunk * blockIdx.x;
   const long long hi = lo + chunk < len ? lo + chunk : len;
-  return {lo, hi};
+  if (vec) {
+#pragma unroll 2
+    for (long long i = lo + (long long)VN * threadIdx.x; i < hi; i += (long long)VN * kThreads)
+      body(i, std::integral_constant<int, VN>{});
+  } else {
+    for (long long i = lo + threadIdx.x; i < hi; i += kThreads) body(i, std::integral_constant<int, 1>{});
+  }
 }
 
 __device__ __forceinline__ void put_partial(double v, double* part) {
@@ -60,11 +103,15 @@ __device__ __forceinline__ void put_partial(double v, double* part) {
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_dot(const T* __restrict__ a, const T* __restrict__ b, long long len,
                                                   double* __restrict__ part) {
-  const Slice s = slice_of(len);
   const T* ab = a + (long long)blockIdx.y * len;
   const T* bb = b + (long long)blockIdx.y * len;
   double acc = 0.0;
-  for (long long i = s.lo + threadIdx.x; i < s.hi; i += kThreads) acc += (double)ab[i] * (double)bb[i];
+  for_slice<T>(len, [&](long long i, auto nc) {
+    constexpr int N = decltype(nc)::value;
+    const auto x = ld<T, N>(ab + i), y = ld<T, N>(bb + i);
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc += (double)x.v[j] * (double)y.v[j];
+  });
   put_partial(acc, part);
 }
 
@@ -72,15 +119,20 @@ __global__ void __launch_bounds__(kThreads) k_dot(const T* __restrict__ a, const
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_resid(T* __restrict__ r, const T* __restrict__ q, long long len,
                                                     const CglsScalars* __restrict__ sc, double* __restrict__ part) {
-  const Slice s = slice_of(len);
   const long long base = (long long)blockIdx.y * len;
   const double alpha = sc[blockIdx.y].alpha;
   double acc = 0.0;
-  for (long long i = s.lo + threadIdx.x; i < s.hi; i += kThreads) {
-    const T v = (T)((double)r[base + i] - alpha * (double)q[base + i]);
-    r[base + i] = v;
-    acc += (double)v * (double)v;
-  }
+  for_slice<T>(len, [&](long long i, auto nc) {
+    constexpr int N = decltype(nc)::value;
+    auto rv = ld<T, N>(r + base + i);
+    const auto qv = ld<T, N>(q + base + i);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      rv.v[j] = (T)((double)rv.v[j] - alpha * (double)qv.v[j]);
+      acc += (double)rv.v[j] * (double)rv.v[j];
+    }
+    st<T, N>(r + base + i, rv);
+  });
   put_partial(acc, part);
 }
 
@@ -88,14 +140,21 @@ __global__ void __launch_bounds__(kThreads) k_resid(T* __restrict__ r, const T* 
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_update_mp(T* __restrict__ m, T* __restrict__ p, const T* __restrict__ s,
                                                         long long len, const CglsScalars* __restrict__ sc) {
-  const Slice sl = slice_of(len);
   const long long base = (long long)blockIdx.y * len;
   const double alpha = sc[blockIdx.y].alpha, beta = sc[blockIdx.y].beta;
-  for (long long i = sl.lo + threadIdx.x; i < sl.hi; i += kThreads) {
-    const double pv = (double)p[base + i];
-    m[base + i] = (T)((double)m[base + i] + alpha * pv);
-    p[base + i] = (T)((double)s[base + i] + beta * pv);
-  }
+  for_slice<T>(len, [&](long long i, auto nc) {
+    constexpr int N = decltype(nc)::value;
+    auto mv = ld<T, N>(m + base + i), pv = ld<T, N>(p + base + i);
+    const auto sv = ld<T, N>(s + base + i);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double pj = (double)pv.v[j];
+      mv.v[j] = (T)((double)mv.v[j] + alpha * pj);
+      pv.v[j] = (T)((double)sv.v[j] + beta * pj);
+    }
+    st<T, N>(m + base + i, mv);
+    st<T, N>(p + base + i, pv);
+  });
 }
 
 // damped, first pass: m += alpha p; s -= damp2 m; part = s . s
@@ -103,17 +162,22 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_damp_s(T* __restrict__ m, const T* __restrict__ p, T* __restrict__ s,
                                                      long long len, const CglsScalars* __restrict__ sc, double damp2,
                                                      double* __restrict__ part) {
-  const Slice sl = slice_of(len);
   const long long base = (long long)blockIdx.y * len;
   const double alpha = sc[blockIdx.y].alpha;
   double acc = 0.0;
-  for (long long i = sl.lo + threadIdx.x; i < sl.hi; i += kThreads) {
-    const T mv = (T)((double)m[base + i] + alpha * (double)p[base + i]);
-    m[base + i] = mv;
-    const T sv = (T)((double)s[base + i] - damp2 * (double)mv);
-    s[base + i] = sv;
-    acc += (double)sv * (double)sv;
-  }
+  for_slice<T>(len, [&](long long i, auto nc) {
+    constexpr int N = decltype(nc)::value;
+    auto mv = ld<T, N>(m + base + i), sv = ld<T, N>(s + base + i);
+    const auto pv = ld<T, N>(p + base + i);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      mv.v[j] = (T)((double)mv.v[j] + alpha * (double)pv.v[j]);
+      sv.v[j] = (T)((double)sv.v[j] - damp2 * (double)mv.v[j]);
+      acc += (double)sv.v[j] * (double)sv.v[j];
+    }
+    st<T, N>(m + base + i, mv);
+    st<T, N>(s + base + i, sv);
+  });
   put_partial(acc, part);
 }
 
@@ -121,11 +185,16 @@ __global__ void __launch_bounds__(kThreads) k_damp_s(T* __restrict__ m, const T*
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_update_p(T* __restrict__ p, const T* __restrict__ s, long long len,
                                                        const CglsScalars* __restrict__ sc) {
-  const Slice sl = slice_of(len);
   const long long base = (long long)blockIdx.y * len;
   const double beta = sc[blockIdx.y].beta;
-  for (long long i = sl.lo + threadIdx.x; i < sl.hi; i += kThreads)
-    p[base + i] = (T)((double)s[base + i] + beta * (double)p[base + i]);
+  for_slice<T>(len, [&](long long i, auto nc) {
+    constexpr int N = decltype(nc)::value;
+    auto pv = ld<T, N>(p + base + i);
+    const auto sv = ld<T, N>(s + base + i);
+#pragma unroll
+    for (int j = 0; j < N; ++j) pv.v[j] = (T)((double)sv.v[j] + beta * (double)pv.v[j]);
+    st<T, N>(p + base + i, pv);
+  });
 }
 
 // one warp per item: fixed-order sum of nblk partials
@@ -173,9 +242,9 @@ inline dim3 vec_grid(int batch, int nblk) { return dim3((unsigned)nblk, (unsigne
 }  // namespace
 
 int cgls_blocks(long long len, int batch, int nsm) {
-  // about 8 resident blocks per SM over the whole batch, at least 2048
-  // elements per block, at most 1024 blocks per item
-  long long want = (8LL * nsm + batch - 1) / batch;
+  // about 16 blocks per SM over the whole batch (two waves of 8 resident),
+  // at least 2048 elements per block, at most 1024 blocks per item
+  long long want = (16LL * nsm + batch - 1) / batch;
   const long long cap = (len + 2047) / 2048;
   if (want > cap) want = cap;
   if (want > 1024) want = 1024;

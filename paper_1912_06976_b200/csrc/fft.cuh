@@ -306,6 +306,9 @@ constexpr bool has_twr(int q) {
 #ifndef BTTB_TWGEN
 #define BTTB_TWGEN 1
 #endif
+#ifndef BTTB_TWGEN_F32
+#define BTTB_TWGEN_F32 BTTB_TWGEN  // fp32 kernels are issue-bound rather than L1-bound
+#endif
 template <int R> struct TwQ {
   static constexpr int Q = R >= 16 ? 4 : R >= 8 ? 4 : R >= 4 ? 2 : 1;
 };
@@ -336,7 +339,7 @@ __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx
   using V = cplx<T>;
   constexpr int NB = E / R;
   constexpr int STRIDE = L / (NS * R);
-  constexpr bool GEN = BTTB_TWGEN && PP && NS > 1 && R >= 4;
+  constexpr bool GEN = (sizeof(T) == 8 ? BTTB_TWGEN : BTTB_TWGEN_F32) && PP && NS > 1 && R >= 4;
   // When a thread's blocks b sit at k = t + NT*b (NT*NB <= NS), the twiddle
   // w^(r*k) of block b is block 0's times the constant w_Q^(r*b), Q = NS*R/NT:
   // one table load per r instead of NB (the table loads are L1 wavefronts,
