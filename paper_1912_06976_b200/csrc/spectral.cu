@@ -370,6 +370,92 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   }
 }
 
+// Double-buffered forward column stage (plans whose column input fits the
+// first half of the transform, nvalid <= L/2, as for every zero-padded
+// embedding at L >= 2n-1): the next layer's Y column is loaded straight into
+// registers (E/2 elements per thread) while the team transforms the current
+// one, and the spectrum columns rotate through TWO shared buffers, so each
+// bulk copy is issued a whole layer ahead of its use instead of during the
+// current layer's FFT.  Shared: [exchange Ls][S0 L][S1 L][2 mbarriers].
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_db(ColFwdArgs a, FFTDesc<typename PL::Scalar> d) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L, EH = E / 2;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = (PL::slots(L) + 1) & ~1;
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* sbuf = sm + Ls;  // two spectrum buffers of L
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + 2 * L);
+  const int t = threadIdx.x;
+  const int kx = blockIdx.x, b = blockIdx.y;
+  const int K = a.K, nv = a.nvalid;
+  const uint32_t sbytes = L * sizeof(V);
+  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const uint64_t pol = policy_evict_first();
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    for (int i = 0; i < 2 && i < K; ++i) {
+      mbar_arrive_expect_tx(&bars[i], sbytes);
+      tma_load(sbuf + i * L, Sb + (long long)i * a.s_rstride, sbytes, &bars[i], pol);
+    }
+  }
+  V yn[EH];
+#pragma unroll
+  for (int k = 0; k < EH; ++k) {
+    const int q = t + NT * k;
+    yn[k] = q < nv ? __ldcs(Yb + q) : mkc<V>(T(0), T(0));
+  }
+  __syncthreads();
+  V acc[E], v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
+  for (int r = 0; r < K; ++r) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = k < EH ? yn[k] : mkc<V>(T(0), T(0));
+    if (r + 1 < K) {
+      const V* yr = Yb + (long long)(r + 1) * a.y_rstride;
+#pragma unroll
+      for (int k = 0; k < EH; ++k) {
+        const int q = t + NT * k;
+        yn[k] = q < nv ? __ldcs(yr + q) : mkc<V>(T(0), T(0));
+      }
+    }
+    PL::fft(v, sm, t, d);
+    const int bi = r & 1;
+    mbar_wait(&bars[bi], (r >> 1) & 1);
+    const V* sb = sbuf + bi * L;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const V w = sb[t + NT * k];
+      acc[k].x += w.x * v[k].x - w.y * v[k].y;
+      acc[k].y += w.x * v[k].y + w.y * v[k].x;
+    }
+    __syncthreads();
+    if (t == 0 && r + 2 < K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[bi], sbytes);
+      tma_load(sbuf + bi * L, Sb + (long long)(r + 2) * a.s_rstride, sbytes, &bars[bi], pol);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
+  PL::fft(acc, sm, t, d);
+  V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int j = t + NT * k;
+    if (j < a.nout) {
+      V val = conjv(acc[k]);
+      if (a.accumulate) val = val + wc[j];
+      wc[j] = val;
+    }
+  }
+}
+
 template <class PL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDesc<typename PL::Scalar> d) {
   using T = typename PL::Scalar;
@@ -1260,6 +1346,12 @@ template <class T> bool quad_rows() {
   }
 }
 
+// double-buffered forward column stage (k_col_fwd_db): BTTB_FWD_DB=1 opt-in
+bool fwd_db_ok() {
+  static const bool on = getenv("BTTB_FWD_DB") && atoi(getenv("BTTB_FWD_DB")) != 0;
+  return on;
+}
+
 bool tma_ok() {
   static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
   return ok;
@@ -1564,6 +1656,15 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
           (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
+        if (fwd_db_ok() && 2 * a.nvalid <= d.L && PL::E % 2 == 0) {
+          auto kern = k_col_fwd_db<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
+          const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + 2 * d.L) * esz + 16;
+          cudaError_t e = set_smem(kern, smem);
+          if (e != cudaSuccess) return e;
+          dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
+          kern<<<grd, blk, smem, st>>>(a, d);
+          return cudaGetLastError();
+        }
         auto kern = k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
