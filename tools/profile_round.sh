@@ -10,6 +10,9 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt
 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+python bench.py --config C5 --dtype f32 --cgls 10 --steps 10 > $OUT/cgls_c5.json 2> $OUT/cgls_c5.err
+ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $OUT/launches_cgls_c5.csv python bench.py --config C5 --dtype f32 --cgls 10 --profile-step > $OUT/ncu_cgls.log 2>&1
 for DT in f64 f32; do
   python bench.py --dtype $DT --profile-step --no-cpu-baseline --no-variants --no-e2e > $OUT/plain_$DT.log 2>&1 && \
   ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
