@@ -142,5 +142,15 @@ int main(int argc, char** argv) {
   run<SPlan<double, 16, 16, 16, 16, 8>, 128, 4>(2048, r16, -3, 1025 * 32, 1, reps);
   run<SPlan<float, 20, 80, 20, 20, 5>, 100, 4>(2000, r20, -3, 1001 * 32, 1, reps);
   run<SPlan<float, 16, 16, 16, 16, 8>, 128, 4>(2048, r16, -3, 1025 * 32, 1, reps);
+  // half-length transforms (a zero-padded 2048 = two 1024s): one warp, one
+  // exchange; measured round 1: fp32 832-892 Gpt/s vs 690 for 2048/E=16, fp64
+  // 419-441 vs 357 (1.2-1.3x per point before the split's twiddle pass)
+  const int r1024[] = {32, 32};
+  run<SPlan<float, 32, 16, 32, 32>, 32, 16>(1024, r1024, -2, 2050 * 32, 1, reps);
+  run<SPlan<float, 32, 32, 32, 32>, 32, 16>(1024, r1024, -2, 2050 * 32, 1, reps);
+  run<SPlan<float, 32, 16, 32, 32>, 32, 24>(1024, r1024, -2, 2050 * 32, 1, reps);
+  run<SPlan<double, 32, 16, 32, 32>, 32, 8>(1024, r1024, -2, 2050 * 32, 1, reps);
+  run<SPlan<double, 32, 8, 32, 32>, 32, 8>(1024, r1024, -2, 2050 * 32, 1, reps);
+  run<SPlan<double, 32, 16, 32, 32>, 32, 12>(1024, r1024, -2, 2050 * 32, 1, reps);
   return 0;
 }
