@@ -106,29 +106,47 @@ __device__ __forceinline__ int emb_to_win(int t, int s, int n, int L) {
   return -1;
 }
 
-// Embedding E[ty][tx] (tx contiguous, Ly rows of Lx) for one layer.
-__global__ void k_embed(EmbedArgs a, const double* __restrict__ cm, MagCorners mc, const double* __restrict__ cx,
-                        const double* __restrict__ cy, int ncy, double z1, double z2, GC5 gc, int* flag,
-                        double* __restrict__ out) {
-  const int tx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ty = blockIdx.y;
-  if (tx >= a.Lx) return;
-  const int wa = emb_to_win(tx, a.sx, a.nx, a.Lx);
-  const int wb = emb_to_win(ty, a.sy, a.ny, a.Ly);
-  double v = 0.0;
-  if (wa >= 0 && wb >= 0) {
-    if (a.kind == 0) {
-      int p = wa - (a.sx + a.pxl - 1);
-      int q = wb - (a.sy + a.pyl - 1);
-      p = p < 0 ? -p : p;
-      q = q < 0 ? -q : q;
-      v = grav_entry(cm, ncy, p, q);
-    } else {
-      v = mag_entry(mc, cx, cy, ncy, wa, wb, z1, z2, gc.v);
+// Embedding E[ty][tx] (tx contiguous, Ly rows of Lx) for one layer, in 32 x 32
+// tiles: the corner tables are [a][b] with b (y) contiguous, so lanes run along
+// y while the entries are evaluated (coalesced corner gathers: lanes along x
+// would touch one cache line per lane and per corner load, 24 per magnetic
+// entry), and the tile is written back through shared memory with lanes along
+// x.  Entry values are unchanged (same function of the same inputs).
+constexpr int kEmbTile = 32, kEmbRows = 8;
+__global__ void __launch_bounds__(kEmbTile* kEmbRows)
+    k_embed(EmbedArgs a, const double* __restrict__ cm, MagCorners mc, const double* __restrict__ cx,
+            const double* __restrict__ cy, int ncy, double z1, double z2, GC5 gc, int* flag,
+            double* __restrict__ out) {
+  __shared__ double tile[kEmbTile][kEmbTile + 1];  // [x][y]
+  const int y0 = blockIdx.x * kEmbTile, x0 = blockIdx.y * kEmbTile;
+  const int ty = y0 + threadIdx.x;
+  const int wb = ty < a.Ly ? emb_to_win(ty, a.sy, a.ny, a.Ly) : -1;
+#pragma unroll
+  for (int i = 0; i < kEmbTile / kEmbRows; ++i) {
+    const int xl = threadIdx.y + kEmbRows * i, tx = x0 + xl;
+    const int wa = tx < a.Lx ? emb_to_win(tx, a.sx, a.nx, a.Lx) : -1;
+    double v = 0.0;
+    if (wa >= 0 && wb >= 0) {
+      if (a.kind == 0) {
+        int p = wa - (a.sx + a.pxl - 1);
+        int q = wb - (a.sy + a.pyl - 1);
+        p = p < 0 ? -p : p;
+        q = q < 0 ? -q : q;
+        v = grav_entry(cm, ncy, p, q);
+      } else {
+        v = mag_entry(mc, cx, cy, ncy, wa, wb, z1, z2, gc.v);
+      }
+      flag_nonfinite(v, flag);
     }
-    flag_nonfinite(v, flag);
+    tile[xl][threadIdx.x] = v;
   }
-  out[(long long)ty * a.Lx + tx] = v;
+  __syncthreads();
+  const int tx = x0 + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < kEmbTile / kEmbRows; ++i) {
+    const int yl = threadIdx.y + kEmbRows * i, y = y0 + yl;
+    if (tx < a.Lx && y < a.Ly) out[(long long)y * a.Lx + tx] = tile[threadIdx.x][yl];
+  }
 }
 
 // Window (mx x my, [a][b] with b contiguous; kernels.py:158-184) for one layer.
@@ -181,7 +199,7 @@ cudaError_t launch_corners(int kind, const double* cx, int ncx, const double* cy
 
 cudaError_t launch_embed(const EmbedArgs& a, const double* cm, MagCorners mc, const double* cx, const double* cy,
                          int ncy, double z1, double z2, GC5 gc, int* flag, double* out, cudaStream_t st) {
-  dim3 blk(128), grd((a.Lx + 127) / 128, a.Ly);
+  dim3 blk(kEmbTile, kEmbRows), grd((a.Ly + kEmbTile - 1) / kEmbTile, (a.Lx + kEmbTile - 1) / kEmbTile);
   k_embed<<<grd, blk, 0, st>>>(a, cm, mc, cx, cy, ncy, z1, z2, gc, flag, out);
   return cudaGetLastError();
 }
