@@ -907,12 +907,15 @@ template <class PL> struct RowTile {
   static constexpr int NI = (HX + PL::NT - 1) / PL::NT;  // kx items per thread
   static constexpr int BOXK = HX < kBoxKx ? HX : kBoxKx;  // box extent along kx (the tensor map's)
   static constexpr int NBOX = (HX + BOXK - 1) / BOXK;
+  static constexpr int PER = 128 / (int)sizeof(cplx<typename PL::Scalar>);
+  // kx extent of one staged row when the two rows arrive as separate boxes,
+  // rounded so the second row's tile starts 128-byte aligned
+  static constexpr int SPAN = (NBOX * BOXK + PER - 1) / PER * PER;
   // shared slots (complex) of one team: exchange buffer or staged box, whichever
   // is larger, rounded to 128 bytes (tensor-TMA shared addresses are 128-B aligned)
   static constexpr int slots(int exchange_slots) {
-    constexpr int per = 128 / (int)sizeof(cplx<typename PL::Scalar>);
-    const int n = exchange_slots > 2 * NBOX * BOXK ? exchange_slots : 2 * NBOX * BOXK;
-    return (n + per - 1) / per * per;
+    const int n = exchange_slots > 2 * SPAN ? exchange_slots : 2 * SPAN;
+    return (n + PER - 1) / PER * PER;
   }
 };
 
@@ -925,7 +928,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   using T = typename PL::Scalar;
   using V = cplx<T>;
   using RT = RowTile<PL>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int c = TEAMS > 1 ? threadIdx.x / NT : 0;
   V* sm = reinterpret_cast<V*>(smraw) + (long long)c * RT::slots((PL::slots(L) + 1) & ~1);
@@ -1091,14 +1094,21 @@ __global__ void __launch_bounds__(MAXT, MINB)
   if (t == 0) tma_store_wait_read();
 }
 
-template <class PL, int MAXT, int MINB, int TEAMS, bool QUAD = false>
+// The FFT input is read straight from the staged tile: element n of the
+// packed row pair is z[n] = A[n] + i B[n] (n <= L/2) or conj(A[L-n]) +
+// i conj(B[L-n]) (Hermitian half), so no intermediate exchange-buffer pass.
+// SPLIT (fp64): each row arrives as its own [kx] box (16-byte box rows), so
+// A and B are contiguous arrays and every tile read is conflict-free.
+template <class PL, int MAXT, int MINB, int TEAMS, bool QUAD = false, bool SPLIT = false>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
   static_assert(!QUAD || TEAMS == 2, "a four-row box takes two teams");
+  static_assert(!(QUAD && SPLIT), "split row boxes are per team");
   using T = typename PL::Scalar;
   using V = cplx<T>;
   using RT = RowTile<PL>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI, NBOX = RT::NBOX;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NBOX = RT::NBOX;
+  constexpr int SPAN = RT::SPAN;  // kx extent of one staged row (split boxes)
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tslots = RT::slots((PL::slots(L) + 1) & ~1);
   const int c = TEAMS > 1 ? threadIdx.x / NT : 0;
@@ -1106,7 +1116,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots) + c;
   const int t = threadIdx.x - c * NT, s = blockIdx.y, ja = 2 * (blockIdx.x * TEAMS + c), jb = ja + 1;
   const bool active = ja < a.nrows;
-  V A[NI], B[NI];
+  // A[n] at sA[n * st], B[n] at sB[n * st]
+  const V* sA;
+  const V* sB;
+  int st;
   if constexpr (QUAD) {
     V* stage = reinterpret_cast<V*>(smraw);
     uint64_t* bar0 = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots);
@@ -1118,51 +1131,50 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
     __syncthreads();
     mbar_wait(bar0, 0);
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const int kx = t + NT * i;
-      if (kx < HX) {
-        A[i] = stage[4 * kx + 2 * c];  // out-of-range rows arrive zero-filled
-        B[i] = stage[4 * kx + 2 * c + 1];
-      }
-    }
+    sA = stage + 2 * c;  // out-of-range rows arrive zero-filled
+    sB = stage + 2 * c + 1;
+    st = 4;
   } else {
     if (t == 0 && active) {
       mbar_init(bar, 1);
       fence_mbar_init();
       // every box delivers its full extent (out-of-range rows zero-filled)
       mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * RT::BOXK * 2 * sizeof(V)));
-      for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
+      for (int b = 0; b < NBOX; ++b) {
+        if constexpr (SPLIT) {
+          tma_load_3d(sm + b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
+          tma_load_3d(sm + SPAN + b * RT::BOXK, &imap, 2 * jb, b * RT::BOXK, s, bar);
+        } else {
+          tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
+        }
+      }
     }
     __syncthreads();
     if (active) mbar_wait(bar, 0);
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const int kx = t + NT * i;
-      if (kx < HX) {
-        A[i] = sm[2 * kx];  // out-of-range rows arrive zero-filled
-        B[i] = sm[2 * kx + 1];
-      }
+    if constexpr (SPLIT) {
+      sA = sm;
+      sB = sm + SPAN;
+      st = 1;
+    } else {
+      sA = sm;
+      sB = sm + 1;
+      st = 2;
     }
   }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int kx = t + NT * i;
-    if (kx < HX) {
-      V a0 = A[i], b0 = B[i];
-      if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
-        a0.y = T(0);
-        b0.y = T(0);
-      }
-      sm[PL::slot(kx)] = mkc<V>(a0.x - b0.y, a0.y + b0.x);
-      if (kx >= 1 && kx <= L - HX) sm[PL::slot(L - kx)] = mkc<V>(a0.x + b0.y, b0.x - a0.y);
-    }
-  }
-  __syncthreads();
   V v[E];
 #pragma unroll
-  for (int k = 0; k < E; ++k) v[k] = conjv(sm[PL::slot(t + NT * k)]);
+  for (int k = 0; k < E; ++k) {
+    const int n = t + NT * k;
+    const bool lo = n < HX;
+    const int m = lo ? n : L - n;
+    V a0 = sA[m * st], b0 = sB[m * st];
+    if (m == 0 || 2 * m == L) {  // Hermitian projection (.real semantics)
+      a0.y = T(0);
+      b0.y = T(0);
+    }
+    // conj of z[n]: the inverse FFT runs as conj(fft(conj(.)))
+    v[k] = lo ? mkc<V>(a0.x - b0.y, -(a0.y + b0.x)) : mkc<V>(a0.x + b0.y, a0.y - b0.x);
+  }
   PL::fft(v, sm, t, d);
   const bool vb = jb < a.nrows;
   T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
@@ -1611,10 +1623,27 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
         kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
         return cudaGetLastError();
       }
-      if (t2d_ok() && !a.rowmajor &&
-          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride)) {
+      // BTTB_C2R_SPLIT=1 (fp64 only: fp32 rows would be 8-byte box rows, below
+      // the tensor-TMA minimum): the two rows as separate [kx] boxes, so the
+      // tile reads are conflict-free -- measured slower (C4 fp64 C2R 0.71 vs
+      // 0.69 ms: the half-sector box rows double the L2 requests)
+      static const bool split_env = env_flag("BTTB_C2R_SPLIT", false);
+      if (sizeof(T) == 8 && split_env && t2d_ok() && !a.rowmajor &&
+          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 1)) {
         constexpr int TM = Shape<PL>::t2d_teams;
-        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM>;
+        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM, false, sizeof(T) == 8>;
+        const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        dim3 grd(((a.nrows + 1) / 2 + TM - 1) / TM, a.nslabs);
+        kern<<<grd, TM * PL::NT, smem, st>>>(a, d, imap);
+        return cudaGetLastError();
+      }
+      constexpr bool SPLIT = false;
+      if (t2d_ok() && !a.rowmajor &&
+          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, SPLIT ? 1 : 2)) {
+        constexpr int TM = Shape<PL>::t2d_teams;
+        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM, false, SPLIT>;
         const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
