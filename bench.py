@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
+                    help="1: capture one step (the C-ABI launches on the plan's streams, joined by "
+                         "events) in a CUDA graph and time its replays (single GPU)")
     ap.add_argument("--cgls", type=int, default=0, metavar="ITERS",
                     help="time the device-resident batched CGLS driver instead: one step = ITERS "
                          "iterations (one G*m and one G^T*d each) over the config's batch; under "
@@ -267,6 +270,21 @@ def run_ours(a):
         if world > 1:
             dist.destroy_process_group()
         return
+    run = step
+    if a.graph and world == 1:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap):
+            step()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=cap):
+                step()
+        torch.cuda.synchronize()
+        run = graph.replay
+        for _ in range(3):
+            run()
+        barrier()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.15)
@@ -275,7 +293,7 @@ def run_ours(a):
     barrier()
     e0.record(stream)
     for _ in range(a.steps):
-        step()
+        run()
     e1.record(stream)
     barrier()
     clocks = sampler.stop()
@@ -409,7 +427,8 @@ def run_ours(a):
                    "l2": "inputs larger than L2 (spectra %.2f GB + model %.2f GB per rank)" % (
                        stack.device_bytes / 1e9,
                        x.numel() * bsz / 1e9),
-                   "step": "1 forward (+all-reduce) + 1 transpose (+broadcast)"},
+                   "step": "1 forward (+all-reduce) + 1 transpose (+broadcast)"
+                           + (", CUDA-graph replay" if (a.graph and world == 1) else "")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "frac_of_8TBs_nameplate": achieved / 8000.0,
