@@ -370,6 +370,76 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   }
 }
 
+// Forward column stage without the Y staging buffer (opt-in BTTB_FWD_NOY=1):
+// the layer's Y column is read straight into registers at the start of each
+// layer, so shared memory holds only the exchange buffer and one spectrum
+// column (67 KB at fp64 L=2048) and three CTAs fit an SM (MINB = 3, 168
+// registers) -- the other two CTAs cover the load latency instead of a TMA
+// prefetch.  Shared: [exchange Ls][S L][mbarrier].
+template <class PL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_noy(ColFwdArgs a, FFTDesc<typename PL::Scalar> d) {
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int Ls = (PL::slots(L) + 1) & ~1;
+  V* sm = reinterpret_cast<V*>(smraw);
+  V* sbuf = sm + Ls;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + L);
+  const int t = threadIdx.x;
+  const int kx = blockIdx.x, b = blockIdx.y;
+  const int K = a.K, nv = a.nvalid;
+  const uint32_t sbytes = L * sizeof(V);
+  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
+  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
+  const uint64_t pol = policy_evict_first();
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, sbytes);
+    tma_load(sbuf, Sb, sbytes, bar, pol);
+  }
+  __syncthreads();
+  V acc[E], v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
+  for (int r = 0; r < K; ++r) {
+    const V* yr = Yb + (long long)r * a.y_rstride;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int q = t + NT * k;
+      v[k] = q < nv ? __ldcs(yr + q) : mkc<V>(T(0), T(0));
+    }
+    PL::fft(v, sm, t, d);
+    mbar_wait(bar, r & 1);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const V w = sbuf[t + NT * k];
+      acc[k].x += w.x * v[k].x - w.y * v[k].y;
+      acc[k].y += w.x * v[k].y + w.y * v[k].x;
+    }
+    __syncthreads();
+    if (t == 0 && r + 1 < K) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, sbytes);
+      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, bar, pol);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
+  PL::fft(acc, sm, t, d);
+  V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int j = t + NT * k;
+    if (j < a.nout) {
+      V val = conjv(acc[k]);
+      if (a.accumulate) val = val + wc[j];
+      wc[j] = val;
+    }
+  }
+}
+
 // Double-buffered forward column stage (plans whose column input fits the
 // first half of the transform, nvalid <= L/2, as for every zero-padded
 // embedding at L >= 2n-1): the next layer's Y column is loaded straight into
@@ -1685,6 +1755,15 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
           (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
+        if (env_flag("BTTB_FWD_NOY", false)) {
+          auto kern = k_col_fwd_noy<PL, Shape<PL>::col_threads, Shape<PL>::tra_minb>;
+          const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * esz + 16;
+          cudaError_t e = set_smem(kern, smem);
+          if (e != cudaSuccess) return e;
+          dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
+          kern<<<grd, blk, smem, st>>>(a, d);
+          return cudaGetLastError();
+        }
         if (fwd_db_ok() && 2 * a.nvalid <= d.L && PL::E % 2 == 0) {
           auto kern = k_col_fwd_db<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
           const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + 2 * d.L) * esz + 16;
