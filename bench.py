@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--reduce", default="data", choices=["data", "spectrum"],
+                    help="N>1 forward/transpose exchange: all-reduce of station vectors (data) or of "
+                         "the partial station half spectra + broadcast of the data spectrum (spectrum)")
     ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
                     help="1: capture one step (the C-ABI launches on the plan's streams, joined by "
                          "events) in a CUDA graph and time its replays (single GPU)")
@@ -226,7 +229,7 @@ def run_ours(a):
         return st, time.perf_counter() - t0
 
     stack, t_build = build(a.dtype)
-    op = ShardedOperator(DeviceOperator(stack))
+    op = ShardedOperator(DeviceOperator(stack), reduce=a.reduce)
     n_r = grid.n_r
     # seeded inputs, generated on the host (the model slice of this rank), resident in HBM
     rng = np.random.default_rng(1000 + rank)
@@ -424,6 +427,9 @@ def run_ours(a):
         "data": "synthetic, seeded host-generated inputs resident in HBM (no dataset exists; SURVEY.md 8(d))",
         "config": {"workload": desc, "fft_shape": list(stack.fft_shape),
                    "layers_per_rank": hi - lo, "parallelism": f"layer-shard x{world}",
+                   "exchange": "none" if world == 1 else (
+                       "all-reduce of partial station vectors + broadcast of the data vector" if a.reduce == "data"
+                       else "all-reduce of partial station half spectra + broadcast of the data half spectrum"),
                    "l2": "inputs larger than L2 (spectra %.2f GB + model %.2f GB per rank)" % (
                        stack.device_bytes / 1e9,
                        x.numel() * bsz / 1e9),

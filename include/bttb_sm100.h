@@ -31,6 +31,7 @@ enum { BTTB_GRAVITY = 0, BTTB_MAGNETIC = 1 };
 enum { BTTB_F64 = 0, BTTB_F32 = 1 };
 enum { BTTB_FORWARD = 0, BTTB_TRANSPOSE = 1 };
 enum { BTTB_DEVICE_PTR = 0, BTTB_HOST_PTR = 1 };
+enum { BTTB_STAGE_ALL = 0, BTTB_STAGE_TO_SPECTRUM = 1, BTTB_STAGE_FROM_SPECTRUM = 2 };
 
 /* Geometry; mirrors GridSpec (grid.py:26-104).  z_blocks has nz+1 entries. */
 typedef struct {
@@ -88,6 +89,20 @@ int bttb_plan_destroy(bttb_plan* plan);
  * asynchronously on `stream`, a cudaStream_t or NULL) or BTTB_HOST_PTR
  * (host memory; copies in and out, synchronous). */
 int bttb_apply(bttb_plan* plan, int mode, const void* x, void* y, int64_t batch, int where, void* stream);
+
+/* Split product for layer-sharded multi-GPU plans (BASELINE north_star: the
+ * per-GPU partial spectra are summed by an NCCL reduce before ONE inverse
+ * transform; the transpose broadcasts the data spectrum).  The split point is
+ * the station half spectrum W: batch x Hx x sy complex (plan dtype), x
+ * frequency by station row, = sum over layers of S_r * FFT(model_r) already
+ * inverse-transformed along y.  Device pointers, asynchronous on `stream`.
+ *   FORWARD   TO_SPECTRUM:   x = model (local layers) -> y = partial W
+ *   FORWARD   FROM_SPECTRUM: x = W (summed over shards) -> y = data
+ *   TRANSPOSE TO_SPECTRUM:   x = data -> y = W (the data's half spectrum)
+ *   TRANSPOSE FROM_SPECTRUM: x = W -> y = model (local layers)
+ * STAGE_ALL is bttb_apply's device path.  Replaces the layer loop of apply
+ * (multiply.py:37-57) split at its cross-layer sum. */
+int bttb_apply_staged(bttb_plan* plan, int mode, int stage, const void* x, void* y, int64_t batch, void* stream);
 
 /* Device-resident batched CGLS -- the inversion loop the paper names as future
  * work (no reference function: the reference stops at apply,

@@ -18,11 +18,12 @@ GRAVITY, MAGNETIC = 0, 1
 F64, F32 = 0, 1
 FORWARD, TRANSPOSE = 0, 1
 DEVICE_PTR, HOST_PTR = 0, 1
+STAGE_ALL, STAGE_TO_SPECTRUM, STAGE_FROM_SPECTRUM = 0, 1, 2
 
 #: every symbol include/bttb_sm100.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
     "bttb_plan_create", "bttb_plan_create_from_spectra", "bttb_plan_create_from_windows", "bttb_plan_destroy",
-    "bttb_apply", "bttb_cgls", "bttb_layer_window",
+    "bttb_apply", "bttb_apply_staged", "bttb_cgls", "bttb_layer_window",
     "bttb_layer_spectrum", "bttb_plan_info", "bttb_gravity_response",
     "bttb_magnetic_response", "bttb_fft_length", "bttb_last_error", "bttb_version",
 )
@@ -67,6 +68,7 @@ def _declare(lib):
                                                   i64, i64, i64, i64, dp]
     lib.bttb_plan_destroy.argtypes = [P]
     lib.bttb_apply.argtypes = [P, ctypes.c_int, P, P, i64, ctypes.c_int, P]
+    lib.bttb_apply_staged.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, i64, P]
     lib.bttb_cgls.argtypes = [P, P, P, i64, ctypes.c_int, ctypes.c_double, ctypes.c_int, P, dp]
     lib.bttb_layer_window.argtypes = [P, i64, dp]
     lib.bttb_layer_spectrum.argtypes = [P, i64, P]
@@ -80,7 +82,7 @@ def _declare(lib):
     lib.bttb_last_error.restype = ctypes.c_char_p
     lib.bttb_version.restype = ctypes.c_char_p
     for name in ("bttb_plan_create", "bttb_plan_create_from_spectra", "bttb_plan_create_from_windows",
-                 "bttb_plan_destroy", "bttb_apply", "bttb_cgls", "bttb_layer_window",
+                 "bttb_plan_destroy", "bttb_apply", "bttb_apply_staged", "bttb_cgls", "bttb_layer_window",
                  "bttb_layer_spectrum", "bttb_plan_info", "bttb_gravity_response",
                  "bttb_magnetic_response"):
         getattr(lib, name).restype = ctypes.c_int

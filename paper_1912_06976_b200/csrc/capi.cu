@@ -278,7 +278,7 @@ struct bttb_plan_s {
   size_t elem = 16;
   void* spectra = nullptr;
   DevBuf work, hin, hout;
-  DevBuf cg;  // CGLS driver workspace (bttb_cgls)
+  DevBuf cg, cg_hist;  // CGLS driver workspace and residual history (bttb_cgls)
   cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
   cudaStream_t stream2 = nullptr;  // second stream: column stages, overlapped with the next chunk's row pass
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -631,9 +631,17 @@ bool use_pipe(const bttb_plan_s* p) {
                               : pipe_supported<float>((int)p->Lx, (int)p->Hx);
 }
 
+// stage: BTTB_STAGE_ALL runs the whole product; the split stages meet at the
+// station half spectrum W[b][kx][j < sy] (x frequency, y space: Hx x sy complex
+// per item) -- forward: TO_SPECTRUM = row R2C + column stage (the plan's layers'
+// partial W, column-inverse-transformed), FROM_SPECTRUM = row C2R of a (summed)
+// W; transpose: TO_SPECTRUM = row R2C of the data, FROM_SPECTRUM = column stage +
+// row C2R into the plan's layers.  x / y are then W where the stage says so.
 template <class T>
-int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st) {
-  if (use_pipe(p)) return run_pipe<T>(p, mode, x, y, batch, st);
+int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st,
+              int stage = BTTB_STAGE_ALL) {
+  if (stage == BTTB_STAGE_ALL && use_pipe(p)) return run_pipe<T>(p, mode, x, y, batch, st);
+  const bool rows_in = stage != BTTB_STAGE_FROM_SPECTRUM, rows_out = stage != BTTB_STAGE_TO_SPECTRUM;
   using V = cplx<T>;
   const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
   const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
@@ -670,7 +678,11 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
     const int gb = (int)std::min<int64_t>(G, batch - b0);
     if (mode == BTTB_FORWARD) {
       const T* xin = static_cast<const T*>(x) + b0 * nloc;
-      for (int64_t r0 = 0; r0 < p->nzl; r0 += K, ++chunk) {
+      // split stages: W lives in the caller's buffer (y for TO_, x for FROM_)
+      V* Wg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b0 * Hx * sy
+              : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b0 * Hx * sy
+                                                  : Wb;
+      for (int64_t r0 = 0; rows_in && r0 < p->nzl; r0 += K, ++chunk) {
         const int k = (int)std::min<int64_t>(K, p->nzl - r0);
         const int bi = chunk % nbuf;
         V* Yb = Ybuf[bi];
@@ -703,7 +715,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.s_rstride = s_rstride;
         ca.lds = (int)p->Ly;
         ca.K = k;
-        ca.W = Wb;
+        ca.W = Wg;
         ca.w_bstride = (long long)Hx * sy;
         ca.ldw = (int)sy;
         ca.nout = (int)sy;
@@ -718,8 +730,9 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         CU(cudaEventRecord(p->ev_aux, sb));
         CU(cudaStreamWaitEvent(sa, p->ev_aux, 0));
       }
+      if (!rows_out) continue;
       RowC2RArgs oa{};
-      oa.in = Wb;
+      oa.in = Wg;
       oa.in_sstride = (long long)Hx * sy;
       oa.ld_in = (int)sy;
       oa.nrows = (int)sy;
@@ -738,6 +751,10 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
       }
     } else {
+      V* Dg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b0 * Hx * sy
+              : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b0 * Hx * sy
+                                                  : Wb;
+      if (rows_in) {
       RowR2CArgs ra{};
       ra.in = static_cast<const T*>(x) + b0 * m;
       ra.in_bstride = m;
@@ -747,7 +764,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       ra.nrows = (int)sy;
       ra.nvalid = (int)sx;
       ra.nslabs = gb;
-      ra.out = Wb;
+      ra.out = Dg;
       ra.out_sstride = (long long)Hx * sy;
       ra.ld_out = (int)sy;
       ra.Hx = (int)Hx;
@@ -757,14 +774,15 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         CU(cudaEventRecord(p->ev_aux, sa));
         CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
       }
+      }
       T* yout = static_cast<T*>(y) + b0 * nloc;
-      for (int64_t r0 = 0; r0 < p->nzl; r0 += K, ++chunk) {
+      for (int64_t r0 = 0; rows_out && r0 < p->nzl; r0 += K, ++chunk) {
         const int k = (int)std::min<int64_t>(K, p->nzl - r0);
         const int bi = chunk % nbuf;
         V* Yb = Ybuf[bi];
         if (pipe) CU(cudaStreamWaitEvent(sb, p->ev_row[bi], 0));  // row pass of chunk-2 done reading Yb
         ColTraArgs ca{};
-        ca.D = Wb;
+        ca.D = Dg;
         ca.d_bstride = (long long)Hx * sy;
         ca.ldd = (int)sy;
         ca.nvalid = (int)sy;
@@ -822,6 +840,7 @@ void destroy_plan(bttb_plan_s* p) {
   p->fy.release();
   p->work.release();
   p->cg.release();
+  p->cg_hist.release();
   if (p->stream) cudaStreamDestroy(p->stream);
   if (p->stream2) cudaStreamDestroy(p->stream2);
   for (int i = 0; i < 2; ++i) {
@@ -1100,8 +1119,12 @@ int bttb_cgls(bttb_plan* p, const void* d, void* m_out, int64_t batch, int iters
     dd = p->hin.p;
     md = p->hout.p;
   }
+  // residual history: device scratch owned by the plan (freed with it)
   double* hist = nullptr;
-  if (resid_norms) CU(cudaMallocAsync(reinterpret_cast<void**>(&hist), sizeof(double) * batch * (iters + 1), st));
+  if (resid_norms) {
+    if ((rc = p->cg_hist.ensure(sizeof(double) * batch * (iters + 1)))) return rc;
+    hist = static_cast<double*>(p->cg_hist.p);
+  }
   CU(cudaEventRecord(p->ev_in, st));
   CU(cudaStreamWaitEvent(p->stream, p->ev_in, 0));
   rc = p->dtype == BTTB_F64
@@ -1115,9 +1138,30 @@ int bttb_cgls(bttb_plan* p, const void* d, void* m_out, int64_t batch, int iters
   if (where == BTTB_HOST_PTR) CU(cudaMemcpyAsync(m_out, md, mbytes, cudaMemcpyDeviceToHost, st));
   if (resid_norms) {
     CU(cudaMemcpyAsync(resid_norms, hist, sizeof(double) * batch * (iters + 1), cudaMemcpyDeviceToHost, st));
-    CU(cudaFreeAsync(hist, st));
   }
   if (where == BTTB_HOST_PTR || resid_norms) CU(cudaStreamSynchronize(st));
+  return BTTB_OK;
+}
+
+int bttb_apply_staged(bttb_plan* p, int mode, int stage, const void* x, void* y, int64_t batch, void* stream) {
+  g_err.clear();
+  if (!p || !x || !y) return fail(BTTB_EINVAL, "null argument");
+  if (mode != BTTB_FORWARD && mode != BTTB_TRANSPOSE)
+    return fail(BTTB_EINVAL, "mode must be 'forward' or 'transpose', got %d", mode);
+  if (stage != BTTB_STAGE_ALL && stage != BTTB_STAGE_TO_SPECTRUM && stage != BTTB_STAGE_FROM_SPECTRUM)
+    return fail(BTTB_EINVAL, "stage must be BTTB_STAGE_ALL, _TO_SPECTRUM or _FROM_SPECTRUM, got %d", stage);
+  if (batch < 0) return fail(BTTB_EINVAL, "batch must be >= 0");
+  if (batch == 0) return BTTB_OK;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CU(cudaEventRecord(p->ev_in, st));
+  CU(cudaStreamWaitEvent(p->stream, p->ev_in, 0));
+  int rc = p->dtype == BTTB_F64 ? run_apply<double>(p, mode, x, y, batch, p->stream, stage)
+                                : run_apply<float>(p, mode, x, y, batch, p->stream, stage);
+  if (rc) return rc;
+  CU(cudaEventRecord(p->ev_out, p->stream));
+  CU(cudaStreamWaitEvent(st, p->ev_out, 0));
   return BTTB_OK;
 }
 

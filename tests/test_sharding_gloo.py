@@ -33,15 +33,48 @@ class OracleLocal:
     def transpose(self, d):
         return torch.from_numpy(O.transpose(self.g, self.tr, d.numpy()))
 
+    # split products in the oracle's own spectral domain (full mx x my spectra,
+    # multiply.py:42-45 / :52-56 split at the cross-layer sum), as real views
+    def forward_spectrum(self, x_local):
+        g, x = self.g, x_local.numpy()
+        acc = np.zeros((g.mx, g.my), dtype=complex)
+        for k in range(len(self.layers)):
+            buf = np.zeros((g.mx, g.my))
+            buf[:g.nx, :g.ny] = x[k * g.n_r:(k + 1) * g.n_r].reshape(g.ny, g.nx).T
+            acc += self.fw[k] * np.fft.fft2(buf)
+        return torch.view_as_real(torch.from_numpy(acc)).contiguous()
 
-def _worker(rank, world, port, kind, out):
+    def from_spectrum(self, w):
+        g = self.g
+        y = np.fft.ifft2(torch.view_as_complex(w.contiguous()).numpy())
+        return torch.from_numpy(y.real[:g.sx, :g.sy].T.ravel().copy())
+
+    def transpose_spectrum(self, d):
+        g = self.g
+        buf = np.zeros((g.mx, g.my))
+        buf[:g.sx, :g.sy] = d.numpy().reshape(g.sy, g.sx).T
+        return torch.view_as_real(torch.from_numpy(np.fft.fft2(buf))).contiguous()
+
+    def empty_spectrum(self, lead, like):
+        return torch.zeros(tuple(lead) + (self.g.mx, self.g.my, 2), dtype=torch.float64)
+
+    def transpose_from_spectrum(self, w):
+        g, vh = self.g, torch.view_as_complex(w.contiguous()).numpy()
+        out = np.empty(len(self.tr) * g.n_r)
+        for k, T in enumerate(self.tr):
+            y = np.fft.ifft2(T * vh)
+            out[k * g.n_r:(k + 1) * g.n_r] = y.real[:g.nx, :g.ny].T.ravel()
+        return torch.from_numpy(out)
+
+
+def _worker(rank, world, port, kind, out, reduce="data"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     g = O.ogrid(7, 5, 5, 1, 2, 2, 0, 1.0, 1.5, (0.0, 1.0, 2.5, 4.0, 4.5, 6.0))
     consts = O.grav_constants() if kind == "gravity" else O.mag_constants(33.0, 47.0, 45000.0)
     lo, hi = partition_layers(g.nz, world)[rank]
-    op = ShardedOperator(OracleLocal(g, kind, consts, lo, hi))
+    op = ShardedOperator(OracleLocal(g, kind, consts, lo, hi), reduce=reduce)
     rng = np.random.default_rng(3)
     x = rng.uniform(size=g.n)
     v = rng.uniform(size=g.m)
@@ -63,12 +96,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("reduce", ["data", "spectrum"])
 @pytest.mark.parametrize("kind", ["gravity", "magnetic"])
-def test_two_rank_layer_sharding_matches_unsharded(kind):
+def test_two_rank_layer_sharding_matches_unsharded(kind, reduce):
     world = 2
     with mp.Manager() as mgr:
         out = mgr.dict()
-        mp.spawn(_worker, args=(world, _free_port(), kind, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), kind, out, reduce), nprocs=world, join=True)
         d, xt = out["d"], out["xt"]
     g = O.ogrid(7, 5, 5, 1, 2, 2, 0, 1.0, 1.5, (0.0, 1.0, 2.5, 4.0, 4.5, 6.0))
     consts = O.grav_constants() if kind == "gravity" else O.mag_constants(33.0, 47.0, 45000.0)
@@ -77,4 +111,7 @@ def test_two_rank_layer_sharding_matches_unsharded(kind):
     x = rng.uniform(size=g.n)
     v = rng.uniform(size=g.m)
     assert O.rel_l2(O.forward(g, fw, x), d) <= 1e-14
-    assert np.array_equal(O.transpose(g, tr, v), xt)
+    if reduce == "data":
+        assert np.array_equal(O.transpose(g, tr, v), xt)
+    else:  # same per-layer arithmetic from the broadcast spectrum
+        assert O.rel_l2(O.transpose(g, tr, v), xt) <= 1e-14
