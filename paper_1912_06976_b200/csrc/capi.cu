@@ -251,6 +251,13 @@ size_t chunk_budget() {
 
 size_t round_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
 
+// column stages: L2 prefetch distance in layers for the streamed Y / S columns
+// (BTTB_L2_AHEAD; 0 or 1 = off)
+int l2_ahead() {
+  static const int v = getenv("BTTB_L2_AHEAD") ? atoi(getenv("BTTB_L2_AHEAD")) : 0;
+  return v;
+}
+
 // overlap the row pass of chunk c+1 with the column stage of chunk c on two
 // streams (double-buffered chunk workspace); opt-in with BTTB_PIPELINE=1
 bool pipelined() {
@@ -722,6 +729,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.accumulate = r0 > 0;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
+        ca.ahead = l2_ahead();
         CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), sb));
         if (pipe) CU(cudaEventRecord(p->ev_col[bi], sb));
         launches += 2;
@@ -798,6 +806,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.nout = (int)ny;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
+        ca.ahead = l2_ahead();
         CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), sb));
         if (pipe) {
           CU(cudaEventRecord(p->ev_col[bi], sb));

@@ -334,6 +334,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], ybytes);
       tma_load(ybuf, Yb + (long long)(r + 1) * a.y_rstride, ybytes, &bars[0], pol);
+      if (a.ahead > 1 && r + a.ahead < K) {
+        l2_prefetch(Yb + (long long)(r + a.ahead) * a.y_rstride, ybytes);
+        l2_prefetch(Sb + (long long)(r + a.ahead) * a.s_rstride, sbytes);
+      }
     }
     PL::fft(v, sm, t, d);
     mbar_wait(&bars[1], r & 1);
@@ -573,6 +577,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], sbytes);
       tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[0], pol);
+      if (a.ahead > 1 && r + a.ahead < K) l2_prefetch(Sb + (long long)(r + a.ahead) * a.s_rstride, sbytes);
     }
     PL::fft(v, sm, t, d);
     V* wc = Wb + (long long)r * a.w_rstride;

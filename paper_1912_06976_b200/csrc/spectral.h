@@ -45,6 +45,7 @@ struct ColFwdArgs {
   void* W;
   long long w_bstride;
   int ldw, nout, accumulate, Hx, nbatch;
+  int ahead;  // > 0: L2-prefetch the Y and S columns of layer r + ahead (TMA kernels)
 };
 
 // Transpose operator, column stage for one chunk of K layers:
@@ -62,6 +63,7 @@ struct ColTraArgs {
   long long w_bstride, w_rstride;
   int ldw, nout, Hx, nbatch;
   int rowmajor;
+  int ahead;  // > 0: L2-prefetch the S column of layer r + ahead (TMA kernels)
 };
 
 // Spectrum build, column stage: S[kx][ky] = scale * FFT_y(Y[kx][0:Ly]) (fp64 FFT,
