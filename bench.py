@@ -335,12 +335,23 @@ def run_ours(a):
                 yo.copy_(t)
             apply_into(stack, "transpose", d_pin.data_ptr(), xo.data_ptr(), batch, host=True)
 
-        e2e_step()
+        # single GPU: the asynchronous host path (BTTB_HOST_ASYNC) -- every step
+        # still copies its inputs in and its results out, but one step's
+        # device-to-host copy overlaps the next step's host-to-device copy
+        e2e_async = world == 1
+        cur = torch.cuda.current_stream().cuda_stream
+
+        def e2e_step_async():
+            apply_into(stack, "forward", x_pin.data_ptr(), yo.data_ptr(), batch, cur, host="async")
+            apply_into(stack, "transpose", d_pin.data_ptr(), xo.data_ptr(), batch, cur, host="async")
+
+        run_e2e = e2e_step_async if e2e_async else e2e_step
+        run_e2e()
         e_steps = max(2, min(a.steps, 10))
         barrier()
         t0 = time.perf_counter()
         for _ in range(e_steps):
-            e2e_step()
+            run_e2e()
         barrier()
         t_e2e = (time.perf_counter() - t0) / e_steps
         if world > 1:
@@ -350,7 +361,9 @@ def run_ours(a):
         e2e = {"value": batch * grid.n / t_e2e, "unit": "voxels/s",
                "h2d_bytes_per_step": int(x_pin.numel() * bsz + d_pin.numel() * bsz),
                "d2h_bytes_per_step": int(yo.numel() * bsz + xo.numel() * bsz),
-               "ms_per_step": 1e3 * t_e2e}
+               "ms_per_step": 1e3 * t_e2e,
+               "path": ("C ABI host pointers, asynchronous (copies of consecutive calls overlap)" if e2e_async
+                        else "C ABI host pointers, synchronous")}
 
     # max over ranks
     vals = torch.tensor([ms, fwd_ms, tra_ms, t_build], device=dev, dtype=torch.float64)

@@ -30,7 +30,7 @@ enum { BTTB_OK = 0, BTTB_EINVAL = -1, BTTB_ECUDA = -2, BTTB_ENONFINITE = -3, BTT
 enum { BTTB_GRAVITY = 0, BTTB_MAGNETIC = 1 };
 enum { BTTB_F64 = 0, BTTB_F32 = 1 };
 enum { BTTB_FORWARD = 0, BTTB_TRANSPOSE = 1 };
-enum { BTTB_DEVICE_PTR = 0, BTTB_HOST_PTR = 1 };
+enum { BTTB_DEVICE_PTR = 0, BTTB_HOST_PTR = 1, BTTB_HOST_ASYNC = 2 };
 enum { BTTB_STAGE_ALL = 0, BTTB_STAGE_TO_SPECTRUM = 1, BTTB_STAGE_FROM_SPECTRUM = 2 };
 
 /* Geometry; mirrors GridSpec (grid.py:26-104).  z_blocks has nz+1 entries. */
@@ -86,8 +86,14 @@ int bttb_plan_destroy(bttb_plan* plan);
  *          sum over the plan's layers; overwritten).
  * TRANSPOSE: x = batch x m, y = batch x (n_r * local layers).
  * where = BTTB_DEVICE_PTR (x, y in device memory of the plan's GPU; runs
- * asynchronously on `stream`, a cudaStream_t or NULL) or BTTB_HOST_PTR
- * (host memory; copies in and out, synchronous). */
+ * asynchronously on `stream`, a cudaStream_t or NULL), BTTB_HOST_PTR
+ * (host memory; copies in and out, synchronous) or BTTB_HOST_ASYNC (host
+ * memory, pinned for overlap; returns at once: x must hold its final values
+ * at call time (its copy is not ordered after `stream`'s pending work) and stay
+ * unchanged, and y be left unread, until the caller synchronises `stream`,
+ * which is ordered after y's copy.  Consecutive calls pipeline:
+ * one call's device-to-host copy overlaps the next call's host-to-device copy
+ * through two plan-owned staging slots). */
 int bttb_apply(bttb_plan* plan, int mode, const void* x, void* y, int64_t batch, int where, void* stream);
 
 /* Split product for layer-sharded multi-GPU plans (BASELINE north_star: the

@@ -17,7 +17,7 @@ BTTB_OK, BTTB_EINVAL, BTTB_ECUDA, BTTB_ENONFINITE, BTTB_ENOMEM = 0, -1, -2, -3, 
 GRAVITY, MAGNETIC = 0, 1
 F64, F32 = 0, 1
 FORWARD, TRANSPOSE = 0, 1
-DEVICE_PTR, HOST_PTR = 0, 1
+DEVICE_PTR, HOST_PTR, HOST_ASYNC = 0, 1, 2
 STAGE_ALL, STAGE_TO_SPECTRUM, STAGE_FROM_SPECTRUM = 0, 1, 2
 
 #: every symbol include/bttb_sm100.h declares (checked by tests/test_capi_symbols.py)

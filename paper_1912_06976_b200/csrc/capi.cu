@@ -289,6 +289,14 @@ struct bttb_plan_s {
   cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
   cudaStream_t stream2 = nullptr;  // second stream: column stages, overlapped with the next chunk's row pass
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  // BTTB_HOST_ASYNC: copy streams and a two-slot ring of device staging
+  // buffers, so one call's device-to-host copy overlaps the next call's
+  // host-to-device copy (full-duplex PCIe) and both overlap compute
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  DevBuf ain[2], aout[2];
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_out_ready[2] = {nullptr, nullptr}, ev_out_free[2] = {nullptr, nullptr}, ev_call = nullptr;
+  int ring = 0;
   cudaEvent_t ev_row[2] = {nullptr, nullptr}, ev_col[2] = {nullptr, nullptr}, ev_aux = nullptr;
   void* window_base = nullptr;
   size_t window_bytes = 0;
@@ -857,6 +865,15 @@ void destroy_plan(bttb_plan_s* p) {
     if (p->ev_col[i]) cudaEventDestroy(p->ev_col[i]);
   }
   if (p->ev_aux) cudaEventDestroy(p->ev_aux);
+  if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+  if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+  for (int i = 0; i < 2; ++i) {
+    p->ain[i].release();
+    p->aout[i].release();
+    for (cudaEvent_t ev : {p->ev_h2d[i], p->ev_in_free[i], p->ev_out_ready[i], p->ev_out_free[i]})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (p->ev_call) cudaEventDestroy(p->ev_call);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   p->hin.release();
@@ -1013,7 +1030,14 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
               cudaEventCreateWithFlags(&p->ev_aux, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 2 && ok; ++i)
       ok = cudaEventCreateWithFlags(&p->ev_row[i], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess;
+           cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->ev_in_free[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->ev_out_ready[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->ev_out_free[i], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&p->ev_call, cudaEventDisableTiming) == cudaSuccess;
     if (!ok) rc = fail(BTTB_ECUDA, "cannot create the plan streams/events");
   }
   if (!rc) {
@@ -1073,6 +1097,32 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   const size_t in_elems = (size_t)batch * (mode == BTTB_FORWARD ? p->nloc() : p->m());
   const size_t out_elems = (size_t)batch * (mode == BTTB_FORWARD ? p->m() : p->nloc());
   const size_t esz = p->elem / 2;
+  if (where == BTTB_HOST_ASYNC) {
+    // ring slot i: H2D (s_h2d) -> compute (plan stream) -> D2H (s_d2h); a slot
+    // is reused only after its previous compute read ain[i] / its previous D2H
+    // read aout[i].  The caller's stream waits for this call's D2H.
+    const int i = p->ring;
+    p->ring ^= 1;
+    int rc;
+    if ((rc = p->ain[i].ensure(in_elems * esz)) || (rc = p->aout[i].ensure(out_elems * esz))) return rc;
+    // the input copy is NOT ordered after st's pending work (that would chain
+    // it behind the previous call's output copy): x must be final at call time
+    CU(cudaStreamWaitEvent(p->s_h2d, p->ev_in_free[i], 0));
+    CU(cudaMemcpyAsync(p->ain[i].p, x, in_elems * esz, cudaMemcpyHostToDevice, p->s_h2d));
+    CU(cudaEventRecord(p->ev_h2d[i], p->s_h2d));
+    CU(cudaStreamWaitEvent(p->stream, p->ev_h2d[i], 0));
+    CU(cudaStreamWaitEvent(p->stream, p->ev_out_free[i], 0));
+    rc = p->dtype == BTTB_F64 ? run_apply<double>(p, mode, p->ain[i].p, p->aout[i].p, batch, p->stream)
+                              : run_apply<float>(p, mode, p->ain[i].p, p->aout[i].p, batch, p->stream);
+    if (rc) return rc;
+    CU(cudaEventRecord(p->ev_in_free[i], p->stream));
+    CU(cudaEventRecord(p->ev_out_ready[i], p->stream));
+    CU(cudaStreamWaitEvent(p->s_d2h, p->ev_out_ready[i], 0));
+    CU(cudaMemcpyAsync(y, p->aout[i].p, out_elems * esz, cudaMemcpyDeviceToHost, p->s_d2h));
+    CU(cudaEventRecord(p->ev_out_free[i], p->s_d2h));
+    CU(cudaStreamWaitEvent(st, p->ev_out_free[i], 0));
+    return BTTB_OK;
+  }
   const void* xd = x;
   void* yd = y;
   if (where == BTTB_HOST_PTR) {
@@ -1082,7 +1132,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
     xd = p->hin.p;
     yd = p->hout.p;
   } else if (where != BTTB_DEVICE_PTR) {
-    return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR or BTTB_HOST_PTR");
+    return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR, BTTB_HOST_PTR or BTTB_HOST_ASYNC");
   }
   // the work runs on the plan's stream (which carries the L2 window), ordered
   // after everything already queued on the caller's stream and before

@@ -75,8 +75,13 @@ def _apply_torch(stack, x, mode, want, other, msg, stream):
 
 
 def apply_into(stack, mode, x_ptr, y_ptr, batch=1, stream_ptr=None, host=False):
-    """Raw-pointer entry (bench / multi-GPU driver): y <- op(x), no validation copies."""
-    where = _lib.HOST_PTR if host else _lib.DEVICE_PTR
+    """Raw-pointer entry (bench / multi-GPU driver): y <- op(x), no validation copies.
+
+    host=False: device pointers; host=True: host pointers, synchronous;
+    host="async": pinned host pointers, returns at once -- x / y are in use
+    until ``stream_ptr`` (default stream if None) is synchronised, and
+    consecutive calls overlap their copies (BTTB_HOST_ASYNC)."""
+    where = _lib.HOST_ASYNC if host == "async" else (_lib.HOST_PTR if host else _lib.DEVICE_PTR)
     _lib.check(_lib.lib().bttb_apply(stack.handle, _MODES[mode], _lib.ctypes.c_void_p(x_ptr),
                                      _lib.ctypes.c_void_p(y_ptr), int(batch), where,
                                      _lib.ctypes.c_void_p(stream_ptr or 0)))

@@ -177,3 +177,28 @@ def test_staged_split_products_match_apply(dtype):
         t_sh = torch.cat([H0.transpose_from_spectrum(wd0), H1.transpose_from_spectrum(wd0)], dim=1)
         assert torch.equal(t_sh, t_all)
         torch.cuda.synchronize()
+
+
+def test_async_host_path_matches_sync():
+    """BTTB_HOST_ASYNC: alternating forward / transpose calls through the two-slot
+    staging ring return exactly what the synchronous host path returns."""
+    import torch
+
+    from paper_1912_06976_b200.multiply import apply_into
+
+    og = O.ogrid(40, 30, 3, 1, 2, 0, 1, 30.0, 30.0, [0.0, 25.0, 60.0, 100.0])
+    grid = B.make_grid(og.sx, og.sy, og.nz, og.pxl, og.pxr, og.pyl, og.pyr, og.dx, og.dy, og.z)
+    rng = np.random.default_rng(4)
+    xs = [torch.tensor(rng.uniform(0, 1, og.n)).pin_memory() for _ in range(3)]
+    vs = [torch.tensor(rng.normal(0, 1, og.m)).pin_memory() for _ in range(3)]
+    with B.build_transform_stack(grid, B.KernelParams.magnetic(5.0, 65.0, 50000.0)) as st:
+        ys = [torch.empty(og.m, dtype=torch.float64).pin_memory() for _ in range(3)]
+        ts = [torch.empty(og.n, dtype=torch.float64).pin_memory() for _ in range(3)]
+        s = torch.cuda.current_stream().cuda_stream
+        for k in range(3):
+            apply_into(st, "forward", xs[k].data_ptr(), ys[k].data_ptr(), 1, s, host="async")
+            apply_into(st, "transpose", vs[k].data_ptr(), ts[k].data_ptr(), 1, s, host="async")
+        torch.cuda.synchronize()
+        for k in range(3):
+            np.testing.assert_array_equal(ys[k].numpy(), B.apply(st, xs[k].numpy(), "forward"))
+            np.testing.assert_array_equal(ts[k].numpy(), B.apply(st, vs[k].numpy(), "transpose"))
