@@ -289,13 +289,15 @@ struct bttb_plan_s {
   cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
   cudaStream_t stream2 = nullptr;  // second stream: column stages, overlapped with the next chunk's row pass
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  // BTTB_HOST_ASYNC: copy streams and a two-slot ring of device staging
-  // buffers, so one call's device-to-host copy overlaps the next call's
-  // host-to-device copy (full-duplex PCIe) and both overlap compute
+  // BTTB_HOST_ASYNC: copy streams and a ring of device staging slots, so one
+  // call's device-to-host copy overlaps the next calls' host-to-device copies
+  // (full-duplex PCIe) and both overlap compute; four slots let alternating
+  // forward / transpose calls each double-buffer their input
+  static constexpr int kRing = 4;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  DevBuf ain[2], aout[2];
-  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
-  cudaEvent_t ev_out_ready[2] = {nullptr, nullptr}, ev_out_free[2] = {nullptr, nullptr}, ev_call = nullptr;
+  DevBuf ain[kRing], aout[kRing];
+  cudaEvent_t ev_h2d[kRing] = {}, ev_in_free[kRing] = {}, ev_out_ready[kRing] = {}, ev_out_free[kRing] = {};
+  cudaEvent_t ev_call = nullptr;
   int ring = 0;
   cudaEvent_t ev_row[2] = {nullptr, nullptr}, ev_col[2] = {nullptr, nullptr}, ev_aux = nullptr;
   void* window_base = nullptr;
@@ -867,7 +869,7 @@ void destroy_plan(bttb_plan_s* p) {
   if (p->ev_aux) cudaEventDestroy(p->ev_aux);
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
   if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < bttb_plan_s::kRing; ++i) {
     p->ain[i].release();
     p->aout[i].release();
     for (cudaEvent_t ev : {p->ev_h2d[i], p->ev_in_free[i], p->ev_out_ready[i], p->ev_out_free[i]})
@@ -1030,8 +1032,9 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
               cudaEventCreateWithFlags(&p->ev_aux, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 2 && ok; ++i)
       ok = cudaEventCreateWithFlags(&p->ev_row[i], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < bttb_plan_s::kRing && ok; ++i)
+      ok = cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&p->ev_in_free[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&p->ev_out_ready[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&p->ev_out_free[i], cudaEventDisableTiming) == cudaSuccess;
@@ -1102,7 +1105,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
     // is reused only after its previous compute read ain[i] / its previous D2H
     // read aout[i].  The caller's stream waits for this call's D2H.
     const int i = p->ring;
-    p->ring ^= 1;
+    p->ring = (p->ring + 1) % bttb_plan_s::kRing;
     int rc;
     if ((rc = p->ain[i].ensure(in_elems * esz)) || (rc = p->aout[i].ensure(out_elems * esz))) return rc;
     // the input copy is NOT ordered after st's pending work (that would chain
