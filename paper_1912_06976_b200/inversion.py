@@ -11,7 +11,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["cgls"]
+__all__ = ["cgls", "cgls_into"]
 
 
 def cgls(stack, d, iters=10, damp=0.0, stream=None, history=True):
@@ -62,3 +62,12 @@ def cgls(stack, d, iters=10, damp=0.0, stream=None, history=True):
     if hist is not None:
         hist = hist.reshape(shape + (int(iters) + 1,))
     return out, hist
+
+
+def cgls_into(stack, d_ptr, m_ptr, batch, iters, damp=0.0, stream_ptr=None, host=False):
+    """Raw-pointer entry (bench): m <- CGLS(d), device pointers or (host=True)
+    host pointers -- pinned for full copy bandwidth -- with a synchronous return."""
+    c = _lib.ctypes
+    _lib.check(_lib.lib().bttb_cgls(stack.handle, c.c_void_p(d_ptr), c.c_void_p(m_ptr), int(batch), int(iters),
+                                    float(damp), _lib.HOST_PTR if host else _lib.DEVICE_PTR,
+                                    c.c_void_p(stream_ptr or 0), None))
