@@ -65,6 +65,27 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def init_dist(world, local):
+    """One process per GPU over NCCL.  Test knobs (not for measurements):
+    BTTB_BENCH_DEVICE pins every rank to one device and BTTB_BENCH_BACKEND=gloo
+    swaps the backend, so the N > 1 host logic runs on a single-GPU box
+    (ranks share the GPU, their kernels never wait on one another)."""
+    import torch
+    import torch.distributed as dist
+
+    dev_env = os.environ.get("BTTB_BENCH_DEVICE")
+    idx = int(dev_env) if dev_env is not None else local
+    torch.cuda.set_device(idx)
+    dev = torch.device("cuda", idx)
+    if world > 1:
+        backend = os.environ.get("BTTB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -206,10 +227,7 @@ def run_ours(a):
     rank, world, local = dist_env()
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     cfg = a.config
     desc, batch = workload(cfg, O)
     og = O.config_grid(cfg)
@@ -226,7 +244,7 @@ def run_ours(a):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st = B.build_transform_stack(grid, params, dtype="float64" if dtype == "f64" else "float32",
-                                     device=local, layers=(lo, hi))
+                                     device=dev.index, layers=(lo, hi))
         torch.cuda.synchronize()
         return st, time.perf_counter() - t0
 
@@ -290,7 +308,7 @@ def run_ours(a):
         for _ in range(3):
             run()
         barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.15)
     stream = torch.cuda.current_stream()
@@ -542,10 +560,7 @@ def run_cgls(a):
     rank, world, local = dist_env()
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     cfg, iters = a.config, a.cgls
     desc, batch = workload(cfg, O)
     og = O.config_grid(cfg)
@@ -560,7 +575,7 @@ def run_cgls(a):
     bsz = 8 if a.dtype == "f64" else 4
     t0 = time.perf_counter()
     stack = B.build_transform_stack(grid, params, dtype="float64" if a.dtype == "f64" else "float32",
-                                    device=local)
+                                    device=dev.index)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     # data of the batch: G applied to seeded N(0, 0.1) models (the C5 recipe) plus noise
@@ -606,7 +621,7 @@ def run_cgls(a):
         for _ in range(3):
             run()
         barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.15)
     stream = torch.cuda.current_stream()
