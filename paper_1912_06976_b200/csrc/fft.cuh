@@ -469,6 +469,11 @@ template <class T, int E_, int PAD, bool PP, int... Rs>
 struct SPlanT {
   using Scalar = T;
   static constexpr bool kPerPass = PP;
+  static constexpr int kPad = PAD;
+  // radices 16/16/8 (L = 2048, 128 threads): the row R2C pass runs its last
+  // radix-8 pass on mirrored butterfly pairs (k_row_r2c_t2d)
+  static constexpr bool kR16x16x8 = sizeof...(Rs) == 3 && E_ == 16 && ((Rs == 16 || Rs == 8) && ...) &&
+                                    (Rs * ...) == 2048;
   static constexpr bool kStatic = true;
   static constexpr int E = E_;
   static constexpr int L = (Rs * ...);

@@ -29,6 +29,9 @@
 #ifndef ROW_REGS_F32
 #define ROW_REGS_F32 64  // register target of the fp32 row passes: four CTAs per SM (C4 fp32 2.42 -> 2.22 ms/step vs 128)
 #endif
+#ifndef BTTB_R2C_PAIR
+#define BTTB_R2C_PAIR 1  // mirrored last pass + in-register separation in the 2048-point row R2C
+#endif
 #ifndef ROW_REGS_F64
 #define ROW_REGS_F64 128  // register target of the fp64 row passes
 #endif
@@ -1021,6 +1024,60 @@ __global__ void __launch_bounds__(MAXT, MINB)
     const bool inb = i < a.nvalid;
     v[k] = mkc<V>(active && inb ? __ldcs(ra + i) : T(0), vb && inb ? __ldcs(rb + i) : T(0));
   }
+  const T h = T(0.5);
+  if constexpr (PL::kR16x16x8 && PL::kPerPass && BTTB_R2C_PAIR) {
+    // Mirrored last pass: thread t runs the radix-8 butterflies j0 = t and
+    // j1 = 256 - t (t = 0: 128) instead of t and t + 128, so it ends up holding
+    // Z[k] AND Z[L - k] (L - (j0 + 256 r) = j1 + 256 (7 - r)) and separates the
+    // two real rows in registers -- no exchange-buffer store / reload of the
+    // whole spectrum before the tile is staged.
+    sfft<T, E, L, PL::kPad, true, 0, 1, 16, 16>(v, sm, t, PL::table(d));
+    __syncthreads();
+    spass_store<T, E, 16, 16, NT, PL::kPad>(v, sm, t);
+    __syncthreads();
+    const int j1 = t == 0 ? 128 : 256 - t;
+    V u0[8], u1[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      u0[r] = sm[pad_slot<PL::kPad>(t + 256 * r)];
+      u1[r] = sm[pad_slot<PL::kPad>(j1 + 256 * r)];
+    }
+    V w[8];
+    gen_twiddles<V, 8, 256>(w, PL::table(d) + 15 * 16, t);  // w[r] = w_2048^(r t)
+    sfor<1, 8>([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      u0[r] = cmul(u0[r], w[r]);
+      // w^(r (256 - t)) = w_8^r conj(w^(r t)); t = 0 pairs with j1 = 128: w_16^r
+      u1[r] = t == 0 ? twc<16, r>(u1[r]) : twc<8, r>(cmul(u1[r], conjv(w[r])));
+    });
+    dft<8>(u0);
+    dft<8>(u1);  // u0[r] = Z[t + 256 r], u1[r] = Z[j1 + 256 r]
+    __syncthreads();  // every thread has read its inputs: the tile may overwrite the buffer
+    auto put = [&](int kx, V zk, V zm) {
+      const V A = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
+      const V B = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
+      if constexpr (QUAD) {
+        V* stage = reinterpret_cast<V*>(smraw);
+        stage[4 * kx + 2 * c] = A;
+        stage[4 * kx + 2 * c + 1] = B;
+      } else {
+        sm[2 * kx] = A;
+        sm[2 * kx + 1] = B;
+      }
+    };
+    if (t == 0) {
+#pragma unroll
+      for (int r = 0; r <= 4; ++r) put(256 * r, u0[r], u0[(8 - r) & 7]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) put(128 + 256 * r, u1[r], u1[7 - r]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        put(t + 256 * r, u0[r], u1[7 - r]);
+        put(256 - t + 256 * r, u1[r], u0[7 - r]);
+      }
+    }
+  } else {
   PL::fft(v, sm, t, d);
   __syncthreads();
 #pragma unroll
@@ -1031,7 +1088,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
   // contiguous 16-byte lanes (the [kx] x {A, B} pairs at a 32-byte stride cost
   // twice the shared-memory wavefronts); the two lanes of a kx read the same
   // zk / zm (broadcast).
-  const T h = T(0.5);
   constexpr int NE = (2 * HX + NT - 1) / NT;
   V P[NE];
 #pragma unroll
@@ -1052,6 +1108,16 @@ __global__ void __launch_bounds__(MAXT, MINB)
       const int e = t + NT * i;
       if (e < 2 * HX) stage[4 * (e >> 1) + 2 * c + (e & 1)] = P[i];
     }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = t + NT * i;
+      if (e < 2 * HX) sm[e] = P[i];
+    }
+  }
+  }
+  if constexpr (QUAD) {
+    V* stage = reinterpret_cast<V*>(smraw);
     fence_proxy_async();
     __syncthreads();
     if (threadIdx.x == 0 && 4 * (int)blockIdx.x < a.nrows) {
@@ -1060,11 +1126,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
       tma_store_wait_read();
     }
   } else {
-#pragma unroll
-    for (int i = 0; i < NE; ++i) {
-      const int e = t + NT * i;
-      if (e < 2 * HX) sm[e] = P[i];
-    }
     fence_proxy_async();
     __syncthreads();
     if (t == 0 && active) {
