@@ -132,6 +132,8 @@ std::vector<C> per_pass_table(const int* radix, int npass) {
   return out;
 }
 
+struct FFTPlanHost;
+template <class T> const void* tw816(const FFTPlanHost& h);
 struct FFTPlanHost {
   int L = 0;
   RadixPlan p64, p32;
@@ -139,6 +141,8 @@ struct FFTPlanHost {
   float2* tw32 = nullptr;
   double2* twp64 = nullptr;  // per-pass tables of the registered compile-time plans (or null)
   float2* twp32 = nullptr;
+  double2* tw816_64 = nullptr;  // L = 2048: per-pass tables of the 8/16/16 order (mirrored C2R)
+  float2* tw816_32 = nullptr;
 
   int init(int64_t len) {
     L = (int)len;
@@ -172,6 +176,15 @@ struct FFTPlanHost {
       CU(cudaMalloc(&twp32, sizeof(float2) * std::max<size_t>(t.size(), 1)));
       if (!t.empty()) CU(cudaMemcpy(twp32, t.data(), sizeof(float2) * t.size(), cudaMemcpyHostToDevice));
     }
+    if (L == 2048) {
+      const int r816[3] = {8, 16, 16};
+      std::vector<double2> t64 = per_pass_table<double2>(r816, 3);
+      std::vector<float2> t32 = per_pass_table<float2>(r816, 3);
+      CU(cudaMalloc(&tw816_64, sizeof(double2) * t64.size()));
+      CU(cudaMalloc(&tw816_32, sizeof(float2) * t32.size()));
+      CU(cudaMemcpy(tw816_64, t64.data(), sizeof(double2) * t64.size(), cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(tw816_32, t32.data(), sizeof(float2) * t32.size(), cudaMemcpyHostToDevice));
+    }
     return BTTB_OK;
   }
   void release() {
@@ -179,6 +192,10 @@ struct FFTPlanHost {
     if (tw32) cudaFree(tw32);
     if (twp64) cudaFree(twp64);
     if (twp32) cudaFree(twp32);
+    if (tw816_64) cudaFree(tw816_64);
+    if (tw816_32) cudaFree(tw816_32);
+    tw816_64 = nullptr;
+    tw816_32 = nullptr;
     tw64 = nullptr;
     tw32 = nullptr;
     twp64 = nullptr;
@@ -205,6 +222,8 @@ struct FFTPlanHost {
     return d;
   }
 };
+template <> const void* tw816<double>(const FFTPlanHost& h) { return h.tw816_64; }
+template <> const void* tw816<float>(const FFTPlanHost& h) { return h.tw816_32; }
 
 struct DevBuf {
   void* p = nullptr;
@@ -574,6 +593,7 @@ int run_pipe(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cu
       oa.spb = 1;
       oa.ld_out = (int)sx;
       oa.nout = (int)sx;
+      oa.tw_816 = tw816<T>(p->fx);
       CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
     } else {
       RowR2CArgs ra{};
@@ -762,6 +782,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       oa.spb = 1;
       oa.ld_out = (int)sx;
       oa.nout = (int)sx;
+      oa.tw_816 = tw816<T>(p->fx);
       CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), sa));
       launches += 1;
       if (pipe) {  // the next batch group's column stages must not overwrite W early
@@ -836,6 +857,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         oa.ld_out = (int)nx;
         oa.nout = (int)nx;
         oa.rowmajor = ca.rowmajor;
+        oa.tw_816 = tw816<T>(p->fx);
         CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), sa));
         if (pipe) CU(cudaEventRecord(p->ev_row[bi], sa));
         launches += 2;

@@ -1326,6 +1326,117 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
 }
 
+// C2R with a MIRRORED first pass (L = 2048): the inverse runs as the radix
+// order 8/16/16 (plan PLC, per-pass twiddles in a.tw_816), whose first radix-8
+// pass has two butterflies per thread; thread t takes j = t and j = 256 - t
+// (t = 0: 128), whose inputs are mirror images (L - (t + 256 r) = (256 - t) +
+// 256 (7 - r)).  So each staged (A[n], B[n]) pair is read ONCE and yields
+// both z[n] = A + iB and z[L-n] = conj(A) + i conj(B) in registers (the
+// direct-read kernel above reads every tile element twice).
+template <class PL, class PLC, int MAXT, int MINB, int TEAMS, bool QUAD>
+__global__ void __launch_bounds__(MAXT, MINB)
+    k_row_c2r_mirror(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
+  static_assert(!QUAD || TEAMS == 2, "a four-row box takes two teams");
+  static_assert(PLC::L == 2048 && PLC::E == 16 && PL::L == 2048, "mirrored C2R: 2048-point plans");
+  using T = typename PL::Scalar;
+  using V = cplx<T>;
+  using RT = RowTile<PL>;
+  constexpr int E = PLC::E, NT = PLC::NT, L = PLC::L, NBOX = RT::NBOX, PADC = PLC::kPad;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tslots = RT::slots((PLC::slots(L) + 1) & ~1);
+  const int c = TEAMS > 1 ? threadIdx.x / NT : 0;
+  V* sm = reinterpret_cast<V*>(smraw) + (long long)c * tslots;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots) + c;
+  const int t = threadIdx.x - c * NT, s = blockIdx.y, ja = 2 * (blockIdx.x * TEAMS + c), jb = ja + 1;
+  const bool active = ja < a.nrows;
+  const V* sA;
+  const V* sB;
+  int st;
+  if constexpr (QUAD) {
+    V* stage = reinterpret_cast<V*>(smraw);
+    uint64_t* bar0 = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smraw) + (long long)TEAMS * tslots);
+    if (threadIdx.x == 0) {
+      mbar_init(bar0, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar0, (uint32_t)(NBOX * RT::BOXK * 4 * sizeof(V)));
+      for (int b = 0; b < NBOX; ++b) tma_load_3d(stage + 4 * b * RT::BOXK, &imap, 8 * blockIdx.x, b * RT::BOXK, s, bar0);
+    }
+    __syncthreads();
+    mbar_wait(bar0, 0);
+    sA = stage + 2 * c;
+    sB = stage + 2 * c + 1;
+    st = 4;
+  } else {
+    if (t == 0 && active) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * RT::BOXK * 2 * sizeof(V)));
+      for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
+    }
+    __syncthreads();
+    if (active) mbar_wait(bar, 0);
+    sA = sm;
+    sB = sm + 1;
+    st = 2;
+  }
+  // conj(z[n]) and conj(z[L-n]) from one staged pair (the inverse runs as
+  // conj(fft(conj(.)))); n = 0 and n = L/2 are their own mirrors and get the
+  // Hermitian projection (.real semantics)
+  auto zpair = [&](int n, V& zn, V& zm) {
+    V a0 = sA[n * st], b0 = sB[n * st];
+    if (n == 0 || 2 * n == L) {
+      a0.y = T(0);
+      b0.y = T(0);
+    }
+    zn = mkc<V>(a0.x - b0.y, -(a0.y + b0.x));
+    zm = mkc<V>(a0.x + b0.y, a0.y - b0.x);
+  };
+  const int j1 = t == 0 ? 128 : 256 - t;
+  V u0[8], u1[8];
+  if (t == 0) {
+#pragma unroll
+    for (int r = 0; r <= 4; ++r) {
+      V zn, zm;
+      zpair(256 * r, zn, zm);
+      u0[r] = zn;
+      if (r != 0 && r != 4) u0[8 - r] = zm;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) zpair(128 + 256 * r, u1[r], u1[7 - r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      zpair(t + 256 * r, u0[r], u1[7 - r]);
+      zpair(256 - t + 256 * r, u1[r], u0[7 - r]);
+    }
+  }
+  dft<8>(u0);  // pass 1 (NS = 1): no twiddles
+  dft<8>(u1);
+  __syncthreads();  // every thread has read the tile: the exchange may overwrite it
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    sm[pad_slot<PADC>(8 * t + r)] = u0[r];
+    sm[pad_slot<PADC>(8 * j1 + r)] = u1[r];
+  }
+  __syncthreads();
+  V v[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) v[k] = sm[pad_slot<PADC>(t + NT * k)];
+  sfft<T, E, L, PADC, true, 0, 8, 16, 16>(v, sm, t, static_cast<const V*>(a.tw_816));
+  const bool vb = jb < a.nrows;
+  T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
+  T* oa = out + (long long)(active ? ja : 0) * a.ld_out;
+  T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int i = t + NT * k;
+    if (i < a.nout && active) {
+      __stcs(oa + i, v[k].x);
+      if (vb) __stcs(ob + i, -v[k].y);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Spectrum build, column stage (fp64 FFT, stored as TS, scaled)
 // ---------------------------------------------------------------------------
@@ -1499,6 +1610,14 @@ bool fwd_db_ok() {
   static const bool on = getenv("BTTB_FWD_DB") && atoi(getenv("BTTB_FWD_DB")) != 0;
   return on;
 }
+
+// mirrored-first-pass C2R (k_row_c2r_mirror) for the 2048 plans: default on,
+// BTTB_C2R_MIRROR=0 falls back to the direct-read kernel
+bool c2r_mirror_ok() {
+  static const bool on = env_flag("BTTB_C2R_MIRROR", true);
+  return on;
+}
+#define C2R_MIRROR_PAD(T) (sizeof(T) == 8 ? 8 : 16)  // bank-searched pad of the 8/16/16 exchanges
 
 bool tma_ok() {
   static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
@@ -1751,6 +1870,19 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
       CUtensorMap imap;
       if (t2d_ok() && quad_rows<T>() && !a.rowmajor &&
           encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 4)) {
+        if constexpr (PL::kR16x16x8 && PL::kPerPass) {
+          if (a.tw_816 && c2r_mirror_ok()) {
+            using PLC = SPlanT<T, 16, C2R_MIRROR_PAD(T), true, 8, 16, 16>;
+            auto kern = k_row_c2r_mirror<PL, PLC, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
+            const size_t smem =
+                (size_t)2 * RowTile<PL>::slots((PLC::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
+            cudaError_t e = set_smem(kern, smem);
+            if (e != cudaSuccess) return e;
+            dim3 grd((a.nrows + 3) / 4, a.nslabs);
+            kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
+            return cudaGetLastError();
+          }
+        }
         auto kern = k_row_c2r_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
         const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
         cudaError_t e = set_smem(kern, smem);
@@ -1779,6 +1911,19 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
       if (t2d_ok() && !a.rowmajor &&
           encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, SPLIT ? 1 : 2)) {
         constexpr int TM = Shape<PL>::t2d_teams;
+        if constexpr (PL::kR16x16x8 && PL::kPerPass) {
+          if (a.tw_816 && c2r_mirror_ok()) {
+            using PLC = SPlanT<T, 16, C2R_MIRROR_PAD(T), true, 8, 16, 16>;
+            auto kern = k_row_c2r_mirror<PL, PLC, TM * PL::NT, Shape<PL>::t2d_minb, TM, false>;
+            const size_t smem =
+                (size_t)TM * RowTile<PL>::slots((PLC::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
+            cudaError_t e = set_smem(kern, smem);
+            if (e != cudaSuccess) return e;
+            dim3 grd(((a.nrows + 1) / 2 + TM - 1) / TM, a.nslabs);
+            kern<<<grd, TM * PL::NT, smem, st>>>(a, d, imap);
+            return cudaGetLastError();
+          }
+        }
         auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM, false, SPLIT>;
         const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
         cudaError_t e = set_smem(kern, smem);

@@ -31,6 +31,9 @@ struct RowC2RArgs {
   long long out_bstride, out_sstride;
   int spb, ld_out, nout;
   int rowmajor;
+  // per-pass twiddle tables of the 8/16/16 radix order at L = 2048 (the
+  // mirrored first pass of k_row_c2r_mirror), or null
+  const void* tw_816;
 };
 
 // Forward operator, column stage for one chunk of K layers:
