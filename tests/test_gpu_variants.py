@@ -22,7 +22,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TOL = {"float64": 1e-10, "float32": 1e-5}
 LAYERS = (0, 3)
 VARIANTS = ["BTTB_FWD_DB=1", "BTTB_FWD_NOY=1", "BTTB_C2R_SPLIT=1", "BTTB_FWD_SPLITS=2", "BTTB_LAYER_SPLITS=4",
-            "BTTB_QUAD=0", "BTTB_R2C_PERSIST=1", "BTTB_NO_TMA=1", "BTTB_FFT_POW2=0", "BTTB_L2_AHEAD=3"]
+            "BTTB_QUAD=0", "BTTB_R2C_PERSIST=1", "BTTB_NO_TMA=1", "BTTB_FFT_POW2=0", "BTTB_L2_AHEAD=3",
+            "BTTB_C2R_MIRROR=0"]
 
 CHILD = r"""
 import sys, numpy as np
