@@ -22,7 +22,7 @@ for DT in f64 f32; do
       --log-file $OUT/traffic_$DT.csv python bench.py --dtype $DT --profile-step --no-cpu-baseline --no-variants --no-e2e > $OUT/ncu2_$DT.log 2>&1
 done
 ncu --profile-from-start off --set full --import-source on --cache-control none --clock-control none \
-    -k regex:"k_col_fwd|k_col_tra|k_row_r2c_t2d|k_row_c2r_t2d" -c 6 \
+    -k regex:"k_col_fwd|k_col_tra|k_row_r2c_t2d|k_row_c2r_t2d|k_row_c2r_mirror" -c 6 \
     -o $OUT/full_f64 python bench.py --profile-step --no-cpu-baseline --no-variants --no-e2e > $OUT/ncu3.log 2>&1
 ncu -i $OUT/full_f64.ncu-rep --page raw --csv > $OUT/full_f64_raw.csv 2>/dev/null
 ncu -i $OUT/full_f64.ncu-rep --page details --csv > $OUT/full_f64_details.csv 2>/dev/null
