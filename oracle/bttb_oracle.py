@@ -23,6 +23,7 @@ __all__ = [
     "layer_window", "embed_window", "transpose_defining_array",
     "build_spectra", "forward", "transpose", "rel_l2", "make_inputs",
     "blob_model", "CONFIGS", "config_grid", "config_kernel", "cgls",
+    "products_chunked", "layer_window_extended",
 ]
 
 #: CODATA gravitational constant (``kernels.py:16``).
@@ -402,6 +403,66 @@ def forward_threaded(g, fw, x, pool):
 def transpose_threaded(g, tr, v, pool):
     parts = list(pool.map(lambda T: transpose(g, [T], v), tr))
     return np.concatenate(parts)
+
+
+def products_chunked(g, kind, consts, x, v, pool, chunk=16):
+    """G x and G^T v over ALL layers of a large grid with bounded memory.
+
+    The reference builds both full spectrum stacks and then loops over layers
+    (transform.py:91-104, multiply.py:37-57); this runs the same per-layer
+    arithmetic chunk by chunk (at most ``chunk`` layers' spectra alive, both
+    stacks) with the layers of a chunk threaded.  Per-layer results are
+    identical to the serial loop; the forward partials are summed chunk by
+    chunk (layer order kept within a chunk).  Returns (d, xt, timings) with
+    the build / forward / transpose seconds.
+    """
+    import time
+
+    x = np.asarray(x, dtype=float)
+    v = np.asarray(v, dtype=float)
+    d = np.zeros(g.m)
+    xt = np.empty(g.n)
+    tb = tf = tt = 0.0
+    for lo in range(0, g.nz, chunk):
+        idx = list(range(lo, min(g.nz, lo + chunk)))
+        t0 = time.perf_counter()
+        fw, tr = build_spectra_threaded(g, kind, consts, idx, pool)
+        t1 = time.perf_counter()
+        d += forward_threaded(g, fw, x[lo * g.n_r:(lo + len(idx)) * g.n_r], pool)
+        t2 = time.perf_counter()
+        xt[lo * g.n_r:(lo + len(idx)) * g.n_r] = transpose_threaded(g, tr, v, pool)
+        t3 = time.perf_counter()
+        tb, tf, tt = tb + t1 - t0, tf + t2 - t1, tt + t3 - t2
+        del fw, tr
+    return d, xt, {"build_s": tb, "fwd_s": tf, "tra_s": tt}
+
+
+def layer_window_extended(g, kind, consts, layer):
+    """Extended-precision (x87 long double, 64-bit significand) response window.
+
+    ACCURACY REFERENCE, not a restatement: the same closed forms as
+    :func:`layer_window` evaluated in ``np.longdouble`` (sqrt, log, arctan2
+    and every product/sum), then rounded once to float64.  The magnetic
+    atan2 sums of deep C4 layers cancel ~1e5-fold, so the reference's fp64
+    entries carry ~1e-11 relative error there while these carry ~1e-15: a
+    truth against which the reference's own accuracy and the GPU's can both
+    be measured (tests/test_gpu_headline.py).
+    """
+    ld = np.longdouble
+    z1, z2 = ld(g.z[layer]), ld(g.z[layer + 1])
+    if kind == "gravity":
+        cx, cy = corner_vectors(g, "sym")
+        q = gravity_corner_sum(z1, z2, cx.astype(ld), cy.astype(ld), ld(consts))
+        ax = np.abs(np.arange(g.mx) - (g.sx + g.pxl - 1))
+        ay = np.abs(np.arange(g.my) - (g.sy + g.pyl - 1))
+        return q[np.ix_(ax, ay)].astype(np.float64)
+    cx, cy = corner_vectors(g, "full")
+    hx = g.sx + max(g.pxl, g.pxr)
+    hy = g.sy + max(g.pyl, g.pyr)
+    sx_ = slice(hx - g.sx - g.pxl, hx + g.sx + g.pxr)
+    sy_ = slice(hy - g.sy - g.pyl, hy + g.sy + g.pyr)
+    w = magnetic_entries(z1, z2, cx[sx_].astype(ld), cy[sy_].astype(ld), np.asarray(consts).astype(ld))
+    return w.astype(np.float64)
 
 
 # --------------------------------------------------------------------------

@@ -42,7 +42,12 @@ def cgls(stack, d, iters=10, damp=0.0, stream=None, history=True):
         din = d.to(dtype=tdt).contiguous()
         batch = 1 if d.dim() == 1 else d.shape[0]
         out = torch.empty(tuple(d.shape[:-1]) + (stack.n_local,), dtype=tdt, device=d.device)
-        st = torch.cuda.current_stream(d.device) if stream is None else stream
+        cur = torch.cuda.current_stream(d.device)
+        st = cur if stream is None else stream
+        if st != cur:  # see multiply._apply_torch: order, keep alive, hand back
+            st.wait_stream(cur)
+            din.record_stream(st)
+            out.record_stream(st)
         xp, yp, where, sp = din.data_ptr(), out.data_ptr(), _lib.DEVICE_PTR, st.cuda_stream
         shape = tuple(d.shape[:-1])
     else:
@@ -59,6 +64,8 @@ def cgls(stack, d, iters=10, damp=0.0, stream=None, history=True):
     _lib.check(_lib.lib().bttb_cgls(stack.handle, c.c_void_p(xp), c.c_void_p(yp), int(batch), int(iters),
                                     float(damp), where, c.c_void_p(sp),
                                     _lib.as_dptr(hist) if history else None))
+    if torch_in and st != cur:
+        cur.wait_stream(st)
     if hist is not None:
         hist = hist.reshape(shape + (int(iters) + 1,))
     return out, hist

@@ -34,7 +34,9 @@ def apply(stack, x, mode, stream=None):
     vectors for transpose (multiply.py:22-58).  numpy input runs host-to-host
     through the C ABI and returns a new float64 (fp32 plan: float32) array;
     a CUDA torch tensor runs device-to-device on ``stream`` (default: the
-    current torch stream) and returns a new tensor.
+    current torch stream) and returns a new tensor; with an explicit stream
+    the work is ordered after the current stream and the current stream is
+    ordered after the result, so the tensor is safe to use on either.
     """
     if mode not in _MODES:
         raise ValueError(f"mode must be 'forward' or 'transpose', got {mode!r}")
@@ -67,10 +69,21 @@ def _apply_torch(stack, x, mode, want, other, msg, stream):
     xin = x.to(dtype=tdt).contiguous()
     out = torch.empty(tuple(x.shape[:-1]) + (other,), dtype=tdt, device=x.device)
     batch = 1 if x.dim() == 1 else x.shape[0]
-    st = torch.cuda.current_stream(x.device) if stream is None else stream
+    cur = torch.cuda.current_stream(x.device)
+    st = cur if stream is None else stream
+    if st != cur:
+        # xin / out are allocated (and xin possibly written) on the current
+        # stream: order the library's work after it, keep both blocks alive
+        # for `st` in the caching allocator, and order the caller's stream
+        # after the result (multiply.py:64)
+        st.wait_stream(cur)
+        xin.record_stream(st)
+        out.record_stream(st)
     _lib.check(_lib.lib().bttb_apply(stack.handle, _MODES[mode], _lib.ctypes.c_void_p(xin.data_ptr()),
                                      _lib.ctypes.c_void_p(out.data_ptr()), batch,
                                      _lib.DEVICE_PTR, _lib.ctypes.c_void_p(st.cuda_stream)))
+    if st != cur:
+        cur.wait_stream(st)
     return out
 
 

@@ -50,7 +50,13 @@ def partition_layers(nz, world):
 
 
 class DeviceOperator:
-    """Device-resident local operator over a TransformStack (no host copies)."""
+    """Device-resident local operator over a TransformStack (no host copies).
+
+    Every tensor handed to the C ABI is checked first (dtype, device,
+    contiguity, trailing length): the library takes raw pointers, so a
+    float64 tensor on an fp32 plan or a strided layer slice would otherwise
+    be read or written out of bounds (parallel.py:62).
+    """
 
     def __init__(self, stack):
         from .multiply import apply_into
@@ -58,20 +64,42 @@ class DeviceOperator:
         self.stack = stack
         self._apply = apply_into
         self.dtype = torch.float64 if stack.dtype.itemsize == 8 else torch.float32
+        self.device = torch.device("cuda", stack.device)
+
+    def _check(self, t, last, what, dims=1):
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{what} must be a torch tensor")
+        if t.dtype != self.dtype:
+            raise ValueError(f"{what} has dtype {t.dtype}, the plan computes in {self.dtype}")
+        if t.device != self.device:
+            raise ValueError(f"{what} lives on {t.device}, the plan on {self.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        if t.dim() < dims or tuple(t.shape[-dims:]) != tuple(last):
+            raise ValueError(f"{what} must end in {tuple(last)}, got {tuple(t.shape)}")
+
+    def _out(self, out, lead, last, like, what):
+        if out is None:
+            return torch.empty(tuple(lead) + tuple(last), dtype=self.dtype, device=like.device)
+        self._check(out, last, what, len(last))
+        if tuple(out.shape[:-len(last)]) != tuple(lead):
+            raise ValueError(f"{what} has leading shape {tuple(out.shape[:-len(last)])}, "
+                             f"expected {tuple(lead)}")
+        return out
 
     def forward(self, x_local, out=None):
         g = self.stack.grid
+        self._check(x_local, (self.stack.n_local,), "x_local")
         batch = 1 if x_local.dim() == 1 else x_local.shape[0]
-        if out is None:
-            out = torch.empty(x_local.shape[:-1] + (g.m,), dtype=self.dtype, device=x_local.device)
+        out = self._out(out, x_local.shape[:-1], (g.m,), x_local, "out")
         self._apply(self.stack, "forward", x_local.data_ptr(), out.data_ptr(), batch,
                     torch.cuda.current_stream(x_local.device).cuda_stream)
         return out
 
     def transpose(self, d, out=None):
+        self._check(d, (self.stack.grid.m,), "d")
         batch = 1 if d.dim() == 1 else d.shape[0]
-        if out is None:
-            out = torch.empty(d.shape[:-1] + (self.stack.n_local,), dtype=self.dtype, device=d.device)
+        out = self._out(out, d.shape[:-1], (self.stack.n_local,), d, "out")
         self._apply(self.stack, "transpose", d.data_ptr(), out.data_ptr(), batch,
                     torch.cuda.current_stream(d.device).cuda_stream)
         return out
@@ -100,28 +128,34 @@ class DeviceOperator:
     def forward_spectrum(self, x_local):
         from . import _lib
 
+        x_local = x_local.contiguous()
+        self._check(x_local, (self.stack.n_local,), "x_local")
         out = torch.empty(self.spectrum_shape(x_local.shape[:-1]), dtype=self.dtype, device=x_local.device)
-        return self._staged("forward", _lib.STAGE_TO_SPECTRUM, x_local.contiguous(), out)
+        return self._staged("forward", _lib.STAGE_TO_SPECTRUM, x_local, out)
 
     def from_spectrum(self, w, out=None):
         from . import _lib
 
-        if out is None:
-            out = torch.empty(w.shape[:-3] + (self.stack.grid.m,), dtype=self.dtype, device=w.device)
-        return self._staged("forward", _lib.STAGE_FROM_SPECTRUM, w.contiguous(), out)
+        w = w.contiguous()
+        self._check(w, self.spectrum_shape(), "w", 3)
+        out = self._out(out, w.shape[:-3], (self.stack.grid.m,), w, "out")
+        return self._staged("forward", _lib.STAGE_FROM_SPECTRUM, w, out)
 
     def transpose_spectrum(self, d):
         from . import _lib
 
+        d = d.contiguous()
+        self._check(d, (self.stack.grid.m,), "d")
         out = torch.empty(self.spectrum_shape(d.shape[:-1]), dtype=self.dtype, device=d.device)
-        return self._staged("transpose", _lib.STAGE_TO_SPECTRUM, d.contiguous(), out)
+        return self._staged("transpose", _lib.STAGE_TO_SPECTRUM, d, out)
 
     def transpose_from_spectrum(self, w, out=None):
         from . import _lib
 
-        if out is None:
-            out = torch.empty(w.shape[:-3] + (self.stack.n_local,), dtype=self.dtype, device=w.device)
-        return self._staged("transpose", _lib.STAGE_FROM_SPECTRUM, w.contiguous(), out)
+        w = w.contiguous()
+        self._check(w, self.spectrum_shape(), "w", 3)
+        out = self._out(out, w.shape[:-3], (self.stack.n_local,), w, "out")
+        return self._staged("transpose", _lib.STAGE_FROM_SPECTRUM, w, out)
 
 
 class ShardedOperator:
@@ -140,6 +174,11 @@ class ShardedOperator:
 
     def _multi(self):
         return dist.is_initialized() and dist.get_world_size(self.group) > 1
+
+    def _root(self):
+        """Global rank of the group's rank 0 (broadcast's ``src`` is global;
+        ADVICE r1: parallel.py:157)."""
+        return 0 if self.group is None else dist.get_global_rank(self.group, 0)
 
     def forward(self, x_local, out=None):
         if self.reduce == "spectrum":
@@ -160,9 +199,9 @@ class ShardedOperator:
             else:
                 w = self.local.empty_spectrum(d.shape[:-1], d)
             if self._multi():
-                dist.broadcast(w, src=0, group=self.group)
+                dist.broadcast(w, src=self._root(), group=self.group)
             return self.local.transpose_from_spectrum(w, out) if out is not None else \
                 self.local.transpose_from_spectrum(w)
         if self._multi():
-            dist.broadcast(d, src=0, group=self.group)
+            dist.broadcast(d, src=self._root(), group=self.group)
         return self.local.transpose(d, out) if out is not None else self.local.transpose(d)

@@ -121,7 +121,21 @@ class TransformStack:
         return out
 
     def layer_window(self, layer):
-        """GPU-generated response window of a (global) layer, (mx, my) float64."""
+        """Response window of a (global) layer, (mx, my) float64.
+
+        Plans built from kernel constants regenerate it on the GPU
+        (``bttb_layer_window``).  Plans loaded from a file carry no kernel
+        constants (``params is None``): their window is recovered from the
+        cached half spectrum itself (:func:`_window_from_spectrum`), so
+        ``forward`` / ``transpose`` / ``save_stack(format="reference")`` of a
+        loaded stack reproduce the file's operator.
+        """
+        if self.params is None:
+            if not self.layer_begin <= layer < self.layer_end:
+                raise ValueError(f"layer {layer} outside this plan's layers "
+                                 f"[{self.layer_begin}, {self.layer_end})")
+            return _window_from_spectrum(self.layer_spectrum(layer - self.layer_begin),
+                                         self.grid, self.fft_shape)
         out = np.empty(self.grid.embed_shape)
         _lib.check(_lib.lib().bttb_layer_window(self.handle, int(layer), _lib.as_dptr(out)))
         return out
@@ -197,6 +211,22 @@ def _embedding(window, sx, sy):
 def _window_from_embedding(T, sx, sy):
     """Inverse of :func:`_embedding`: the response window a T^circ holds."""
     return np.roll(T, (-sx, -sy), axis=(0, 1))[::-1, ::-1]
+
+
+def _window_from_spectrum(S, grid, fft_shape):
+    """Response window held by a cached half spectrum (host, off the hot path).
+
+    The plan caches S = fft2(E) / (Lx*Ly), half along x, where E is the
+    zero-gap embedding at the FFT lengths: E[t] = h(-pxl-t) for t < sx and
+    E[L-u] = h(u-pxl) for 0 < u < nx (per axis; transform.py:85-88 at L >= mx).
+    Window entry a holds offset a-(sx+pxl-1), so window[a] = E[sx-1-a] for
+    a < sx and window[sx-1+u] = E[L-u].
+    """
+    lx, ly = fft_shape
+    E = np.fft.irfft(np.fft.ifft(np.asarray(S, dtype=np.complex128), axis=1), n=lx, axis=0) * (lx * ly)
+    ix = np.concatenate([np.arange(grid.sx - 1, -1, -1), lx - np.arange(1, grid.nx)])
+    iy = np.concatenate([np.arange(grid.sy - 1, -1, -1), ly - np.arange(1, grid.ny)])
+    return np.ascontiguousarray(E[np.ix_(ix, iy)])
 
 
 def _reference_stacks(stack):

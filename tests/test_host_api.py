@@ -146,11 +146,11 @@ def test_bench_csv_schema_matches_reference_columns():
 
     assert CSV_COLUMNS == ("schema_version", "problem", "padding", "kernel", "path", "phase",
                            "trials", "mean_seconds", "mean_rel_error_vs_dense", "m", "n", "seed")
-    rec = BenchRecord(problem=2, padding=0.1, kernel="gravity", path="transform-gpu", phase="forward",
+    rec = BenchRecord(problem=2, padding=0.1, kernel="gravity", path="transform", phase="forward",
                       trials=5, mean_seconds=1.5e-3, mean_rel_error=None, m=1500, n=8640, seed=0)
     lines = bench_csv_text([rec]).splitlines()
     assert lines[0] == ",".join(CSV_COLUMNS)
-    assert lines[1] == "1,2,0.1,gravity,transform-gpu,forward,5,1.500000000e-03,,1500,8640,0"
+    assert lines[1] == "1,2,0.1,gravity,transform,forward,5,1.500000000e-03,,1500,8640,0"
 
 
 def test_cli_bench_rejects_bad_problem_index(capsys):
