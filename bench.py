@@ -102,6 +102,38 @@ def workload(cfg, O):
     return desc, batch
 
 
+def csrc_digest():
+    """sha256 (16 hex) of the CUDA sources: ties a committed ncu traffic figure to the kernels it measured."""
+    import hashlib
+
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_1912_06976_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".h")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(cfg, dtype):
+    """DRAM bytes per application from the committed ncu capture (profiles/traffic.json:
+    dram__bytes_read.sum + dram__bytes_write.sum over one application's launches), or None
+    when that capture was taken on different kernel sources than the ones running."""
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(tpath) as fh:
+            rec = json.load(fh).get(f"{cfg}_{dtype}")
+    except (OSError, ValueError):
+        return None, None
+    if not isinstance(rec, dict):
+        return None, None
+    src = {"profile": rec.get("profile"), "csrc_sha": rec.get("csrc_sha"), "current_csrc_sha": csrc_digest()}
+    if rec.get("csrc_sha") != src["current_csrc_sha"]:
+        src["stale"] = True
+        return None, src
+    return rec.get("bytes_per_apply"), src
+
+
 def algorithmic_bytes(g, b, batch):
     """B = b*batch*(n+m) + b*nz*mx*my per application."""
     return b * batch * (g.n + g.m) + b * g.nz * g.mx * g.my
@@ -187,28 +219,75 @@ def cpu_sample(cfg, steps, warmup, layers_hint=None):
             "fwd_s": tf / steps, "tra_s": tt / steps, "build_s": t_build}
 
 
+def cpu_full(cfg, x, v, threads=None):
+    """The reference algorithm (oracle port) over EVERY layer of the config on
+    the given inputs: all spectra built, one forward and one transpose, layers
+    threaded on the host cores with bounded memory (O.products_chunked).
+    Returns (d, xt, info) with the per-phase seconds -- the bench's parity
+    oracle and its full-configuration CPU baseline in one pass."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import bttb_oracle as O
+
+    cores = threads or os.cpu_count() or 1
+    g = O.config_grid(cfg)
+    kind, consts = O.config_kernel(cfg)
+    with ThreadPoolExecutor(cores) as pool:
+        d, xt, tm = O.products_chunked(g, kind, consts, x, v, pool)
+    tm["cores"] = cores
+    return d, xt, tm
+
+
 def run_reference(a):
+    """The reference's CPU path on the FULL configuration (every layer of
+    C4): the reference algorithm (pinned oracle port -- the reference is pure
+    numpy) with its two complex128 spectrum stacks built once, then per step
+    one forward and one transpose over all layers, layers threaded over the
+    host cores.  Steps are capped at 10 and warm-up at 1 so the run stays
+    within a few minutes (each C4 step is ~7 s of 16-thread CPU work)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import bttb_oracle as O
 
     desc, batch = workload(a.config, O)
     cores = os.cpu_count() or 1
-    sample_layers = min(O.CONFIGS[a.config][2], 2 * cores) if a.config in ("C4", "C5") else None
+    g = O.config_grid(a.config)
+    kind, consts = O.config_kernel(a.config)
+    x, d = O.make_inputs(a.config, g, batch=1)
     steps = max(1, min(a.steps, 10))
-    warm = max(1, min(a.warmup, 2))
-    r = cpu_sample(a.config, steps, warm, sample_layers)
+    warm = max(0, min(a.warmup, 1))
+    with ThreadPoolExecutor(cores) as pool:
+        t0 = time.perf_counter()
+        fw, tr = O.build_spectra_threaded(g, kind, consts, list(range(g.nz)), pool)
+        t_build = time.perf_counter() - t0
+        for _ in range(warm):
+            O.forward_threaded(g, fw, x[0], pool)
+            O.transpose_threaded(g, tr, d[0], pool)
+        tf = tt = 0.0
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.forward_threaded(g, fw, x[0], pool)
+            t1 = time.perf_counter()
+            O.transpose_threaded(g, tr, d[0], pool)
+            tf += t1 - t0
+            tt += time.perf_counter() - t1
+    value = g.n * steps / (tf + tt)
+    sample = (f"{a.config}: all {g.nz} layers, 1 model, both complex128 spectrum stacks resident "
+              f"({2 * g.nz * g.mx * g.my * 16 / 1e9:.1f} GB), numpy pocketfft (reference algorithm, oracle "
+              f"port), {cores} threads over layers; build {t_build:.1f} s, fwd {1e3 * tf / steps:.0f} ms, "
+              f"tra {1e3 * tt / steps:.0f} ms per step")
     line = {
-        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "voxels/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "voxels/s",
         "n_gpus": a.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 * (r["fwd_s"] + r["tra_s"]), "higher_is_better": True,
+        "ms_per_step": 1e3 * (tf + tt) / steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic, seeded (SURVEY.md 8(d))",
-        "config": {"workload": desc, "sample": r["sample"]},
-        "cpu_baseline": {"value": r["value"], "unit": "voxels/s", "cores": r["cores"], "kind": "port",
-                         "sample": r["sample"]},
-        "e2e": {"value": r["value"], "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": desc, "sample": sample, "same_config": True},
+        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -432,6 +511,7 @@ def run_ours(a):
     ms, fwd_ms, tra_ms, t_build = vals.tolist()
 
     variants = {}
+    variant_out = {}
     if not a.no_variants and cfg == "C4":
         other = "f32" if a.dtype == "f64" else "f64"
         st2, tb2 = build(other)
@@ -464,6 +544,8 @@ def run_ours(a):
         variants[other] = {"ms_per_step": ms2, "value": batch * grid.n / (ms2 * 1e-3),
                            "roofline_frac": 2 * algorithmic_bytes(og, b2, batch) / (ms2 * 1e-3) / 1e9 / peak,
                            "build_s": tb2}
+        variant_out[other] = (y2.reshape(-1, grid.m)[0].double().cpu().numpy(),
+                              xt2.reshape(-1, xt2.shape[-1])[0].double().cpu().numpy())
         st2.close()
 
     if rank != 0:
@@ -473,18 +555,36 @@ def run_ours(a):
     peak, peak_kind = peaks()
     B_apply = algorithmic_bytes(og, bsz, batch)
     achieved = 2 * B_apply / (ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as fh:
-                traffic = json.load(fh).get(f"{cfg}_{a.dtype}")
-        except (OSError, ValueError):
-            traffic = None
+    traffic, traffic_src = measured_traffic(cfg, a.dtype)
     cpu = None
+    parity = None
     if not a.no_cpu_baseline and world == 1:
-        cores = os.cpu_count() or 1
-        cpu = cpu_sample(cfg, 1, 1, min(nz, cores) if cfg in ("C4", "C5") else None)
+        if cfg in ("C4", "C5"):
+            # the reference algorithm over EVERY layer on the bench's own inputs:
+            # parity oracle of the benched step and full-configuration CPU baseline
+            y_gpu = y[0].double().cpu().numpy()
+            xt_gpu = xt[0].double().cpu().numpy()
+            d_ref, xt_ref, tm = cpu_full(cfg, xh[0], dh[0])
+            from oracle import bttb_oracle as O2
+            gate = 1e-10 if a.dtype == "f64" else 1e-5
+            parity = {"fwd_rel_l2": O2.rel_l2(d_ref, y_gpu), "tra_rel_l2": O2.rel_l2(xt_ref, xt_gpu),
+                      "gate": gate,
+                      "oracle": f"reference algorithm (oracle port) over all {nz} layers on the benched inputs "
+                                f"(model seed 1000, data seed 1), fp64"}
+            parity["pass"] = bool(parity["fwd_rel_l2"] <= gate and parity["tra_rel_l2"] <= gate)
+            for name, (yv, xv) in variant_out.items():
+                g2 = 1e-10 if name == "f64" else 1e-5
+                variants[name]["parity"] = {"fwd_rel_l2": O2.rel_l2(d_ref, yv), "tra_rel_l2": O2.rel_l2(xt_ref, xv),
+                                            "gate": g2}
+            cpu = {"value": grid.n / (tm["fwd_s"] + tm["tra_s"]), "unit": "voxels/s", "cores": tm["cores"],
+                   "kind": "port",
+                   "sample": (f"{cfg}: all {nz} layers (the full benched configuration, not extrapolated), "
+                              f"1 model, numpy pocketfft (reference algorithm, oracle port), {tm['cores']} "
+                              f"threads over layers, spectra built chunk by chunk; build {tm['build_s']:.1f} s, "
+                              f"fwd {1e3 * tm['fwd_s']:.0f} ms, tra {1e3 * tm['tra_s']:.0f} ms")}
+        else:
+            cpu = cpu_sample(cfg, 1, 1, None)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "sample")} | {"kind": "port"}
     line = {
         "metric": METRIC,
         "value": batch * grid.n / (ms * 1e-3),
@@ -511,14 +611,14 @@ def run_ours(a):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "frac_of_8TBs_nameplate": achieved / 8000.0,
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_apply": B_apply,
                      "kernel": "fused operator (row R2C -> column FFT*S accumulate -> column IFFT -> row C2R)"},
         "fwd_ms": fwd_ms, "tra_ms": tra_ms, "build_s": t_build,
         "fwd_voxels_per_s": batch * grid.n / (fwd_ms * 1e-3),
         "tra_voxels_per_s": batch * grid.n / (tra_ms * 1e-3),
-        "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "sample")}
-        | {"kind": "port"},
+        "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": e2e,
         "clocks": clocks,
         "gpu_launches": int((launch_fwd + launch_tra) * a.steps),

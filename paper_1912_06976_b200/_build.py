@@ -23,6 +23,7 @@ UNITS = {
     "entries.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"],
     "spectral.cu": ["-Xptxas", "-v"] if os.environ.get("BTTB_PTXAS_VERBOSE") else [],
     "cgls.cu": [],
+    "fused.cu": ["-Xptxas", "-v"] if os.environ.get("BTTB_PTXAS_VERBOSE") else [],
     "capi.cu": [],
 }
 
@@ -41,6 +42,20 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _includes(path, seen=None):
+    """Local headers a source includes, transitively (its rebuild dependencies)."""
+    import re
+
+    seen = set() if seen is None else seen
+    for name in re.findall(r'^#include "([^"]+)"', open(path).read(), re.M):
+        for d in (CSRC, INC):
+            f = os.path.join(d, name)
+            if os.path.exists(f) and f not in seen:
+                seen.add(f)
+                _includes(f, seen)
+    return seen
+
+
 def build(force=False, verbose=False, variant=None, defines=()):
     """Build the library; ``variant``/``defines`` (development experiments)
     build into build/<variant>/ with extra -D flags instead of in-tree; load
@@ -51,14 +66,12 @@ def build(force=False, verbose=False, variant=None, defines=()):
         LIB = os.path.join(BUILD, "libbttb_sm100.so")
         force = True
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
-    headers.append(os.path.join(INC, "bttb_sm100.h"))
     objs = []
     for unit, flags in UNITS.items():
         src = os.path.join(CSRC, unit)
         obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
         objs.append(obj)
-        if force or _stale(obj, [src] + headers + [__file__]):
+        if force or _stale(obj, [src] + sorted(_includes(src)) + [__file__]):
             cmd = [nvcc()] + ARCH + COMMON + list(defines) + flags + ["-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)

@@ -19,6 +19,7 @@
 #include "bttb_sm100.h"
 #include "cgls.h"
 #include "entries.h"
+#include "fused.h"
 #include "spectral.h"
 
 using namespace bttb;
@@ -303,6 +304,7 @@ struct bttb_plan_s {
   FFTPlanHost fx, fy;
   size_t elem = 16;
   void* spectra = nullptr;
+  bool fused = false;  // fused whole-stack kernels (fused.cu); spectra stored ky-split
   DevBuf work, hin, hout;
   DevBuf cg, cg_hist;  // CGLS driver workspace and residual history (bttb_cgls)
   cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
@@ -668,6 +670,148 @@ bool use_pipe(const bttb_plan_s* p) {
                               : pipe_supported<float>((int)p->Lx, (int)p->Hx);
 }
 
+// Fused whole-stack kernels (fused.cu): per vector, forward = fused kernel
+// (row transforms + column stages of every layer, L2 ring, TMEM accumulators)
+// writing the station half spectrum W[kx][j < sy], then the row C2R of the
+// stations; transpose = row R2C of the data into W, then the fused kernel.
+// The split stages meet at W exactly as in the staged path (run_apply).
+template <class T>
+int run_fused(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st, int stage) {
+  using V = cplx<T>;
+  const bool rows_in = stage != BTTB_STAGE_FROM_SPECTRUM, rows_out = stage != BTTB_STAGE_TO_SPECTRUM;
+  const FFTDesc<T> dx = p->fx.desc<T>();
+  const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, m = p->m(), nloc = p->nloc();
+  static const int look_env = getenv("BTTB_FUSED_AHEAD") ? atoi(getenv("BTTB_FUSED_AHEAD")) : 2;
+  const int D = std::max(1, look_env), NB = D + 1;
+  const int64_t ring_ld = (ny + 1) & ~int64_t(1);
+  const size_t ring = round_up((size_t)NB * Hx * ring_ld * sizeof(V), 4096);
+  const size_t wbytes = round_up((size_t)Hx * sy * sizeof(V), 4096);
+  const int ncnt = fused_counter_ints((int)p->nzl);
+  const size_t cbytes = round_up((size_t)ncnt * sizeof(int), 4096);
+  int rc;
+  // BTTB_FUSED_STATS=1: per-warp cycle accounting of the last vector, printed to stderr (development aid)
+  static const bool stats_on = getenv("BTTB_FUSED_STATS") && atoi(getenv("BTTB_FUSED_STATS")) != 0;
+  const int nwarps = fused_grid() * fused_warps(std::is_same<T, double>::value);
+  const size_t sbytes = stats_on ? (size_t)nwarps * FZ_NSTAT * sizeof(long long) : 0;
+  if ((rc = p->work.ensure(ring + wbytes + cbytes + sbytes))) return rc;
+  char* base = static_cast<char*>(p->work.p);
+  V* Wb = reinterpret_cast<V*>(base + ring);
+  int* cnt = reinterpret_cast<int*>(base + ring + wbytes);
+  long long* stats = stats_on ? reinterpret_cast<long long*>(base + ring + wbytes + cbytes) : nullptr;
+  if (!p->pipe_err_host) CU(cudaMallocHost(&p->pipe_err_host, sizeof(int)));
+  if (*p->pipe_err_host) return fail(BTTB_ECUDA, "fused kernel deadlock guard tripped in an earlier apply");
+  FusedArgs a{};
+  a.S = p->spectra;
+  a.s_rstride = (long long)Hx * p->Ly;
+  a.ring = base;
+  a.ring_sstride = (long long)Hx * ring_ld;
+  a.ring_ld = (int)ring_ld;
+  a.nb = NB;
+  a.sync = cnt;
+  a.tw = std::is_same<T, double>::value ? (const void*)p->fy.tw64 : (const void*)p->fy.tw32;
+  a.nz = (int)p->nzl;
+  a.nx = (int)nx;
+  a.ny = (int)ny;
+  a.sx = (int)sx;
+  a.sy = (int)sy;
+  a.Hx = (int)Hx;
+  a.npairs = (int)((ny + 1) / 2);
+  a.n_r = p->n_r();
+  a.lookahead = D;
+  a.stats = stats;
+  p->last_K = p->nzl;
+  p->last_G = 1;
+  int64_t launches = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    if (mode == BTTB_FORWARD) {
+      V* Wg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b * Hx * sy
+              : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b * Hx * sy
+                                                  : Wb;
+      if (rows_in) {
+        CU(cudaMemsetAsync(cnt, 0, (size_t)ncnt * sizeof(int), st));
+        a.in = static_cast<const T*>(x) + b * nloc;
+        a.out = Wg;
+        CU(launch_fused<T>(0, a, st));
+        CU(cudaMemcpyAsync(p->pipe_err_host, cnt + ncnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        launches += 1;
+      }
+      if (rows_out) {
+        RowC2RArgs oa{};
+        oa.in = Wg;
+        oa.in_sstride = (long long)Hx * sy;
+        oa.ld_in = (int)sy;
+        oa.nrows = (int)sy;
+        oa.Hx = (int)Hx;
+        oa.nslabs = 1;
+        oa.out = static_cast<T*>(y) + b * m;
+        oa.out_bstride = m;
+        oa.out_sstride = 0;
+        oa.spb = 1;
+        oa.ld_out = (int)sx;
+        oa.nout = (int)sx;
+        oa.tw_816 = tw816<T>(p->fx);
+        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
+        launches += 1;
+      }
+    } else {
+      V* Dg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b * Hx * sy
+              : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b * Hx * sy
+                                                  : Wb;
+      if (rows_in) {
+        RowR2CArgs ra{};
+        ra.in = static_cast<const T*>(x) + b * m;
+        ra.in_bstride = m;
+        ra.in_sstride = 0;
+        ra.spb = 1;
+        ra.ld_in = (int)sx;
+        ra.nrows = (int)sy;
+        ra.nvalid = (int)sx;
+        ra.nslabs = 1;
+        ra.out = Dg;
+        ra.out_sstride = (long long)Hx * sy;
+        ra.ld_out = (int)sy;
+        ra.Hx = (int)Hx;
+        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
+        launches += 1;
+      }
+      if (rows_out) {
+        CU(cudaMemsetAsync(cnt, 0, (size_t)ncnt * sizeof(int), st));
+        a.in = Dg;
+        a.out = static_cast<T*>(y) + b * nloc;
+        CU(launch_fused<T>(1, a, st));
+        CU(cudaMemcpyAsync(p->pipe_err_host, cnt + ncnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        launches += 1;
+      }
+    }
+  }
+  p->last_launches = launches;
+  if (stats_on) {
+    std::vector<long long> hs((size_t)nwarps * FZ_NSTAT);
+    CU(cudaMemcpyAsync(hs.data(), stats, sbytes, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    double mean[FZ_NSTAT] = {0}, mx[FZ_NSTAT] = {0};
+    for (int i = 0; i < nwarps; ++i)
+      for (int j = 0; j < FZ_NSTAT; ++j) {
+        mean[j] += (double)hs[(size_t)i * FZ_NSTAT + j] / nwarps;
+        mx[j] = std::max(mx[j], (double)hs[(size_t)i * FZ_NSTAT + j]);
+      }
+    fprintf(stderr,
+            "[fused %s] per warp mean/max kcycles: total %.0f/%.0f wait %.0f/%.0f grab %.0f/%.0f rows %.0f/%.0f "
+            "(%.2f/%.0f items) cols %.0f/%.0f (%.2f/%.0f items) pro/epi %.0f/%.0f\n",
+            mode == BTTB_FORWARD ? "fwd" : "tra", mean[5] / 1e3, mx[5] / 1e3, mean[0] / 1e3, mx[0] / 1e3,
+            mean[1] / 1e3, mx[1] / 1e3, mean[2] / 1e3, mx[2] / 1e3, mean[6], mx[6], mean[3] / 1e3, mx[3] / 1e3,
+            mean[7], mx[7], mean[4] / 1e3, mx[4] / 1e3);
+  }
+  return BTTB_OK;
+}
+
+// the fused kernels run plans whose geometry they support (fused_supported);
+// BTTB_FUSED=0 keeps the staged kernels
+bool use_fused(const bttb_plan_s* p) {
+  static const bool on = !(getenv("BTTB_FUSED") && atoi(getenv("BTTB_FUSED")) == 0);
+  return on && fused_supported(p->Lx, p->Ly, p->nx, p->ny, p->sx, p->sy);
+}
+
 // stage: BTTB_STAGE_ALL runs the whole product; the split stages meet at the
 // station half spectrum W[b][kx][j < sy] (x frequency, y space: Hx x sy complex
 // per item) -- forward: TO_SPECTRUM = row R2C + column stage (the plan's layers'
@@ -677,6 +821,7 @@ bool use_pipe(const bttb_plan_s* p) {
 template <class T>
 int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st,
               int stage = BTTB_STAGE_ALL) {
+  if (p->fused) return run_fused<T>(p, mode, x, y, batch, st, stage);
   if (stage == BTTB_STAGE_ALL && use_pipe(p)) return run_pipe<T>(p, mode, x, y, batch, st);
   const bool rows_in = stage != BTTB_STAGE_FROM_SPECTRUM, rows_out = stage != BTTB_STAGE_TO_SPECTRUM;
   using V = cplx<T>;
@@ -1074,6 +1219,13 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
       rc = build_spectra(p, host_windows);
     }
   }
+  if (!rc && use_fused(p)) {  // the fused kernels read each warp's ky half contiguously
+    cudaError_t ce = p->dtype == BTTB_F64 ? launch_ky_split<double>(p->spectra, p->nzl * p->Hx, +1, 0)
+                                          : launch_ky_split<float>(p->spectra, p->nzl * p->Hx, +1, 0);
+    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    if (ce != cudaSuccess) rc = fail(BTTB_ECUDA, "spectrum layout: %s", cudaGetErrorString(ce));
+    p->fused = !rc;
+  }
   if (rc) {
     std::string msg = g_err;
     destroy_plan(p);
@@ -1285,6 +1437,17 @@ int bttb_layer_spectrum(bttb_plan* p, int64_t local_layer, void* host_out) {
   DeviceGuard dg(p->device);
   const size_t bytes = (size_t)p->Hx * p->Ly * p->elem;
   CU(cudaMemcpy(host_out, static_cast<char*>(p->spectra) + bytes * local_layer, bytes, cudaMemcpyDeviceToHost));
+  if (p->fused) {  // ky-split rows (fused.h) back to natural ky order
+    std::vector<char> row(p->Ly * p->elem);
+    char* h = static_cast<char*>(host_out);
+    const size_t half = (size_t)(p->Ly / 2) * p->elem;
+    for (int64_t kx = 0; kx < p->Hx; ++kx) {
+      char* r = h + (size_t)kx * p->Ly * p->elem;
+      memcpy(row.data(), r, row.size());
+      for (int64_t ky = 0; ky < p->Ly; ++ky)
+        memcpy(r + ky * p->elem, row.data() + (ky & 1) * half + (size_t)(ky >> 1) * p->elem, p->elem);
+    }
+  }
   return BTTB_OK;
 }
 
