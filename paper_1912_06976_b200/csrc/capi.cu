@@ -805,10 +805,10 @@ int run_fused(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
   return BTTB_OK;
 }
 
-// the fused kernels run plans whose geometry they support (fused_supported);
-// BTTB_FUSED=0 keeps the staged kernels
+// the fused kernels run plans whose geometry they support (fused_supported)
+// when BTTB_FUSED=1 (opt-in while they are slower than the staged kernels)
 bool use_fused(const bttb_plan_s* p) {
-  static const bool on = !(getenv("BTTB_FUSED") && atoi(getenv("BTTB_FUSED")) == 0);
+  static const bool on = getenv("BTTB_FUSED") && atoi(getenv("BTTB_FUSED")) != 0;
   return on && fused_supported(p->Lx, p->Ly, p->nx, p->ny, p->sx, p->sy);
 }
 
