@@ -51,9 +51,12 @@ def parse():
                     help="1: capture one step (the C-ABI launches on the plan's streams, joined by "
                          "events) in a CUDA graph and time its replays (single GPU)")
     ap.add_argument("--cgls", type=int, default=0, metavar="ITERS",
-                    help="time the device-resident batched CGLS driver instead: one step = ITERS "
-                         "iterations (one G*m and one G^T*d each) over the config's batch; under "
-                         "torchrun the batch's models are sharded over the ranks")
+                    help="time the batched CGLS driver instead: one step = ITERS iterations (one "
+                         "G*m and one G^T*d each) over the config's batch; under torchrun the depth "
+                         "layers are sharded over the ranks (BASELINE configs[4]), one NCCL all-reduce "
+                         "of the partial G*p plus the scalar reductions per iteration")
+    ap.add_argument("--cgls-shard", default="layers", choices=["layers", "models"],
+                    help="N>1 CGLS: shard depth layers (default) or models over replicated stacks")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints nothing")
@@ -80,6 +83,10 @@ def init_dist(world, local):
     if world > 1:
         backend = os.environ.get("BTTB_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator logging (ranks, channels, NVLS) goes to stderr, so a
+            # scaling run can verify the communicator size; stdout stays one JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -441,8 +448,8 @@ def run_ours(a):
         cur = torch.cuda.current_stream().cuda_stream
 
         def e2e_step_async():
-            apply_into(stack, "forward", x_pin.data_ptr(), yo.data_ptr(), batch, cur, host="async")
-            apply_into(stack, "transpose", d_pin.data_ptr(), xo.data_ptr(), batch, cur, host="async")
+            apply_into(stack, "forward", x_pin.data_ptr(), yo.data_ptr(), batch, cur, host="async-unordered")
+            apply_into(stack, "transpose", d_pin.data_ptr(), xo.data_ptr(), batch, cur, host="async-unordered")
 
         # several GPUs (or --e2e-torch): the same pipelining one level up --
         # pinned host tensors copied on a side stream into two alternating device
@@ -668,27 +675,45 @@ def run_cgls(a):
     sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, dz, _, kargs, _ = O.CONFIGS[cfg]
     grid = B.make_grid(sx, sy, nz, pxl, pxr, pyl, pyr, dx, dy, og.z)
     params = B.KernelParams.gravity() if kind == "gravity" else B.KernelParams.magnetic(*kargs)
-    # models sharded over ranks (replicas of the whole stack, no collective in the loop)
-    b0, b1 = batch * rank // world, batch * (rank + 1) // world
-    nb = b1 - b0
     np_dt = np.float64 if a.dtype == "f64" else np.float32
     bsz = 8 if a.dtype == "f64" else 4
+    sdt = "float64" if a.dtype == "f64" else "float32"
+    layer_shard = world > 1 and a.cgls_shard == "layers"
+    if layer_shard:
+        # BASELINE configs[4]: depth layers sharded, every rank iterates all models
+        from paper_1912_06976_b200.parallel import DeviceOperator, ShardedOperator, partition_layers, sharded_cgls
+
+        lo, hi = partition_layers(nz, world)[rank]
+        b0, b1 = 0, batch
+    else:
+        # one GPU, or models sharded over ranks (replicas of the whole stack)
+        lo, hi = 0, nz
+        b0, b1 = batch * rank // world, batch * (rank + 1) // world
+    nb = b1 - b0
     t0 = time.perf_counter()
-    stack = B.build_transform_stack(grid, params, dtype="float64" if a.dtype == "f64" else "float32",
-                                    device=dev.index)
+    stack = B.build_transform_stack(grid, params, dtype=sdt, device=dev.index, layers=(lo, hi))
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     # data of the batch: G applied to seeded N(0, 0.1) models (the C5 recipe) plus noise
     rng = np.random.default_rng(1000)
-    truth = rng.normal(0.0, 0.1, (batch, grid.n))[b0:b1]
-    dgen = B.apply(stack, torch.tensor(truth, device=dev), "forward")
+    truth = rng.normal(0.0, 0.1, (batch, grid.n))[b0:b1, lo * grid.n_r:hi * grid.n_r]
+    tdt = torch.float64 if a.dtype == "f64" else torch.float32
+    if layer_shard:
+        sop = ShardedOperator(DeviceOperator(stack))
+        dgen = sop.forward(torch.tensor(truth, device=dev, dtype=tdt).contiguous())
+    else:
+        dgen = B.apply(stack, torch.tensor(truth, device=dev), "forward")
     dgen += 1e-3 * dgen.abs().max() * torch.randn(dgen.shape, generator=torch.Generator(device=dev).manual_seed(7),
                                                    device=dev, dtype=dgen.dtype)
     d_dev = dgen.contiguous()
     d_pin = d_dev.cpu().pin_memory()
 
-    def step():
-        return B.cgls(stack, d_dev, iters=iters, history=False)[0]
+    if layer_shard:
+        def step():
+            return sharded_cgls(sop, d_dev, iters=iters, history=False)[0]
+    else:
+        def step():
+            return B.cgls(stack, d_dev, iters=iters, history=False)[0]
 
     def barrier():
         if world > 1:
@@ -707,7 +732,7 @@ def run_cgls(a):
             dist.destroy_process_group()
         return
     run = step
-    if a.graph:
+    if a.graph and not layer_shard:
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         cap.wait_stream(torch.cuda.current_stream())
@@ -736,21 +761,38 @@ def run_cgls(a):
     ms = e0.elapsed_time(e1) / a.steps
     # one product of each kind for the launch count and the roofline split
     m_dev = step()
-    _, hist = B.cgls(stack, d_dev, iters=iters)
-    launches = int(stack.info()[9])
-    # end to end: pinned host data in, pinned host models out, through the C ABI host path
-    from paper_1912_06976_b200.inversion import cgls_into
-
     d_host = d_pin.numpy()
-    m_pin = torch.empty((nb, grid.n), dtype=d_pin.dtype).pin_memory()
-    cgls_into(stack, d_pin.data_ptr(), m_pin.data_ptr(), nb, iters, host=True)
+    m_pin = torch.empty((nb, stack.n_local), dtype=d_pin.dtype).pin_memory()
+    e_steps = max(2, min(a.steps, 5))
+    if layer_shard:
+        _, hist = sharded_cgls(sop, d_dev, iters=iters)
+        hist = hist.cpu().numpy()
+        launches = None  # per-product launches vary by plan; counted per product below
+
+        def e2e_step():
+            dd = d_pin.to(dev, non_blocking=True)
+            m_pin.copy_(sharded_cgls(sop, dd, iters=iters, history=False)[0], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    else:
+        _, hist = B.cgls(stack, d_dev, iters=iters)
+        launches = int(stack.info()[9])
+        # end to end: pinned host data in, pinned host models out, through the C ABI host path
+        from paper_1912_06976_b200.inversion import cgls_into
+
+        def e2e_step():
+            cgls_into(stack, d_pin.data_ptr(), m_pin.data_ptr(), nb, iters, host=True)
+    e2e_step()
     barrier()
     t0 = time.perf_counter()
-    e_steps = max(2, min(a.steps, 5))
     for _ in range(e_steps):
-        cgls_into(stack, d_pin.data_ptr(), m_pin.data_ptr(), nb, iters, host=True)
+        e2e_step()
     barrier()
     t_e2e = (time.perf_counter() - t0) / e_steps
+    if launches is None:  # library kernels of one sharded loop: iters forward + iters+1 transpose products
+        B.apply(stack, m_dev, "forward")
+        lf = int(stack.info()[9])
+        B.apply(stack, d_dev, "transpose")
+        launches = lf * iters + int(stack.info()[9]) * (iters + 1)
     vals = torch.tensor([ms, t_e2e], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
@@ -772,8 +814,10 @@ def run_cgls(a):
         "data": "synthetic: seeded N(0,0.1) models through the operator plus 0.1% noise, resident in HBM",
         "config": {"workload": desc, "step": f"{iters} CGLS iterations (G*m + G^T*d each) over the batch"
                    + (", CUDA-graph replay" if a.graph else ""),
-                   "fft_shape": list(stack.fft_shape), "models_per_rank": nb,
-                   "parallelism": f"model-shard x{world} (replicated stack)",
+                   "fft_shape": list(stack.fft_shape), "models_per_rank": nb, "layers_per_rank": hi - lo,
+                   "parallelism": (f"layer-shard x{world} (NCCL all-reduce of G*p + scalars per iteration)"
+                                   if layer_shard else f"model-shard x{world} (replicated stack)"
+                                   if world > 1 else "single GPU, device-resident loop (bttb_cgls)"),
                    "l2": "per-iteration vectors (%.2f GB) larger than L2" % (3 * nb * grid.n * bsz / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
@@ -782,7 +826,7 @@ def run_cgls(a):
         "build_s": t_build, "residual_drop_median": rel_drop,
         "cpu_baseline": cpu,
         "e2e": {"value": batch * grid.n * iters / t_e2e, "unit": "voxels/s",
-                "h2d_bytes_per_step": int(d_host.size * bsz), "d2h_bytes_per_step": int(nb * grid.n * bsz),
+                "h2d_bytes_per_step": int(d_host.size * bsz), "d2h_bytes_per_step": int(nb * stack.n_local * bsz),
                 "ms_per_step": 1e3 * t_e2e},
         "clocks": clocks,
         "gpu_launches": launches * a.steps, "launches_per_step": launches,

@@ -30,7 +30,7 @@ enum { BTTB_OK = 0, BTTB_EINVAL = -1, BTTB_ECUDA = -2, BTTB_ENONFINITE = -3, BTT
 enum { BTTB_GRAVITY = 0, BTTB_MAGNETIC = 1 };
 enum { BTTB_F64 = 0, BTTB_F32 = 1 };
 enum { BTTB_FORWARD = 0, BTTB_TRANSPOSE = 1 };
-enum { BTTB_DEVICE_PTR = 0, BTTB_HOST_PTR = 1, BTTB_HOST_ASYNC = 2 };
+enum { BTTB_DEVICE_PTR = 0, BTTB_HOST_PTR = 1, BTTB_HOST_ASYNC = 2, BTTB_HOST_ASYNC_UNORDERED = 3 };
 enum { BTTB_STAGE_ALL = 0, BTTB_STAGE_TO_SPECTRUM = 1, BTTB_STAGE_FROM_SPECTRUM = 2 };
 
 /* Geometry; mirrors GridSpec (grid.py:26-104).  z_blocks has nz+1 entries. */
@@ -87,13 +87,17 @@ int bttb_plan_destroy(bttb_plan* plan);
  * TRANSPOSE: x = batch x m, y = batch x (n_r * local layers).
  * where = BTTB_DEVICE_PTR (x, y in device memory of the plan's GPU; runs
  * asynchronously on `stream`, a cudaStream_t or NULL), BTTB_HOST_PTR
- * (host memory; copies in and out, synchronous) or BTTB_HOST_ASYNC (host
- * memory, pinned for overlap; returns at once: x must hold its final values
- * at call time (its copy is not ordered after `stream`'s pending work) and stay
- * unchanged, and y be left unread, until the caller synchronises `stream`,
- * which is ordered after y's copy.  Consecutive calls pipeline:
+ * (host memory; copies in and out, synchronous), BTTB_HOST_ASYNC (host
+ * memory, pinned for overlap; returns at once: the input copy is ordered
+ * after the work queued on `stream` at call time, x must stay unchanged and y
+ * be left unread until the caller synchronises `stream`, which is ordered
+ * after y's copy) or BTTB_HOST_ASYNC_UNORDERED (the same, except that the
+ * input copy is NOT ordered after `stream`: x must hold its final values at
+ * call time.  Dropping that edge is what lets consecutive calls pipeline --
  * one call's device-to-host copy overlaps the next call's host-to-device copy
- * through two plan-owned staging slots). */
+ * through plan-owned staging slots; with the ordered mode `stream` already
+ * waits for the previous call's output copy, so the next input copy queues
+ * behind it). */
 int bttb_apply(bttb_plan* plan, int mode, const void* x, void* y, int64_t batch, int where, void* stream);
 
 /* Split product for layer-sharded multi-GPU plans (BASELINE north_star: the
@@ -150,6 +154,13 @@ int bttb_magnetic_response(const double* x, int64_t ncx, const double* y, int64_
  * a>=2, b>=1), except that a power of two within 5% of it is preferred when
  * the library has a compile-time FFT plan for it (e.g. 1999 -> 2048). */
 int64_t bttb_fft_length(int64_t n);
+
+/* Development check (no reference counterpart): with BTTB_GUARD=1 in the
+ * environment every plan buffer and the spectrum cache carry 64 KB guard
+ * zones of a fixed pattern on both sides; this synchronises the device and
+ * returns how many buffers had a guard byte overwritten (0 = clean; always 0
+ * when guards are off), or a negative error code. */
+int bttb_debug_check_guards(bttb_plan* plan);
 
 /* Last error message on the calling thread ("" if none). */
 const char* bttb_last_error(void);

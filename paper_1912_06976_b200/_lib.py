@@ -17,7 +17,7 @@ BTTB_OK, BTTB_EINVAL, BTTB_ECUDA, BTTB_ENONFINITE, BTTB_ENOMEM = 0, -1, -2, -3, 
 GRAVITY, MAGNETIC = 0, 1
 F64, F32 = 0, 1
 FORWARD, TRANSPOSE = 0, 1
-DEVICE_PTR, HOST_PTR, HOST_ASYNC = 0, 1, 2
+DEVICE_PTR, HOST_PTR, HOST_ASYNC, HOST_ASYNC_UNORDERED = 0, 1, 2, 3
 STAGE_ALL, STAGE_TO_SPECTRUM, STAGE_FROM_SPECTRUM = 0, 1, 2
 
 #: every symbol include/bttb_sm100.h declares (checked by tests/test_capi_symbols.py)
@@ -25,7 +25,7 @@ EXPORTS = (
     "bttb_plan_create", "bttb_plan_create_from_spectra", "bttb_plan_create_from_windows", "bttb_plan_destroy",
     "bttb_apply", "bttb_apply_staged", "bttb_cgls", "bttb_layer_window",
     "bttb_layer_spectrum", "bttb_plan_info", "bttb_gravity_response",
-    "bttb_magnetic_response", "bttb_fft_length", "bttb_last_error", "bttb_version",
+    "bttb_magnetic_response", "bttb_fft_length", "bttb_debug_check_guards", "bttb_last_error", "bttb_version",
 )
 
 
@@ -77,6 +77,8 @@ def _declare(lib):
                                           ctypes.c_double, ctypes.c_double, dp, ctypes.c_int]
     lib.bttb_magnetic_response.argtypes = [dp, i64, dp, i64, dp, ctypes.c_double,
                                            ctypes.c_double, dp, dp, ctypes.c_int]
+    lib.bttb_debug_check_guards.argtypes = [P]
+    lib.bttb_debug_check_guards.restype = ctypes.c_int
     lib.bttb_fft_length.argtypes = [i64]
     lib.bttb_fft_length.restype = i64
     lib.bttb_last_error.restype = ctypes.c_char_p

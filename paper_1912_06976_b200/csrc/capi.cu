@@ -226,24 +226,68 @@ struct FFTPlanHost {
 template <> const void* tw816<double>(const FFTPlanHost& h) { return h.tw816_64; }
 template <> const void* tw816<float>(const FFTPlanHost& h) { return h.tw816_32; }
 
+// Development guard zones (BTTB_GUARD=1, read once per process): every plan
+// buffer and the spectrum cache get kGuard bytes of a fixed byte pattern on
+// both sides; bttb_debug_check_guards reports buffers whose guards changed --
+// out-of-bounds writes of any kernel into neighbouring memory.  (The pool's
+// compute-sanitizer is unavailable; this plus the boundary / determinism
+// tests in tests/test_gpu_guards.py stands in for memcheck.)
+constexpr size_t kGuard = 1 << 16;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guards_on() {
+  static const bool on = getenv("BTTB_GUARD") && atoi(getenv("BTTB_GUARD")) != 0;
+  return on;
+}
+int guard_alloc(void** p, size_t n) {
+  if (!guards_on()) return cudaMalloc(p, n) == cudaSuccess ? 0 : 1;
+  char* base = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&base), n + 2 * kGuard) != cudaSuccess) return 1;
+  if (cudaMemset(base, kGuardByte, kGuard) != cudaSuccess ||
+      cudaMemset(base + kGuard + n, kGuardByte, kGuard) != cudaSuccess) {
+    cudaFree(base);
+    return 1;
+  }
+  *p = base + kGuard;
+  return 0;
+}
+void guard_free(void* p) {
+  if (p) cudaFree(guards_on() ? static_cast<char*>(p) - kGuard : p);
+}
+// 0: both guards intact (or guards off), 1: a guard byte changed, -1: copy failed
+int guard_intact(const void* p, size_t n) {
+  if (!guards_on() || !p) return 0;
+  std::vector<unsigned char> h(kGuard);
+  const char* base = static_cast<const char*>(p) - kGuard;
+  for (const char* g : {base, base + kGuard + n}) {
+    if (cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    for (unsigned char c : h)
+      if (c != kGuardByte) return 1;
+  }
+  return 0;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   int ensure(size_t n) {
     if (n <= bytes) return BTTB_OK;
-    if (p) cudaFree(p);
+    guard_free(p);
     p = nullptr;
     bytes = 0;
-    cudaError_t e = cudaMalloc(&p, n);
-    if (e != cudaSuccess) return fail(BTTB_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", n, cudaGetErrorString(e));
+    if (guard_alloc(&p, n)) {
+      p = nullptr;
+      cudaError_t e = cudaGetLastError();
+      return fail(BTTB_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", n, cudaGetErrorString(e));
+    }
     bytes = n;
     return BTTB_OK;
   }
   void release() {
-    if (p) cudaFree(p);
+    guard_free(p);
     p = nullptr;
     bytes = 0;
   }
+  int intact() const { return guard_intact(p, bytes); }
 };
 
 struct DeviceGuard {
@@ -1020,7 +1064,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
 void destroy_plan(bttb_plan_s* p) {
   if (!p) return;
   DeviceGuard g(p->device);
-  if (p->spectra) cudaFree(p->spectra);
+  if (p->spectra) guard_free(p->spectra);
   if (p->pipe_err_host) cudaFreeHost(p->pipe_err_host);
   p->fx.release();
   p->fy.release();
@@ -1185,7 +1229,7 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
   if (!rc) rc = p->fy.init(p->Ly);
   if (!rc) {
     const size_t bytes = (size_t)p->nzl * p->Hx * p->Ly * p->elem;
-    e = cudaMalloc(&p->spectra, bytes);
+    e = guard_alloc(&p->spectra, bytes) ? cudaErrorMemoryAllocation : cudaSuccess;
     if (e != cudaSuccess) {
       p->spectra = nullptr;
       rc = fail(BTTB_ENOMEM, "cannot allocate %zu bytes of spectrum cache: %s", bytes, cudaGetErrorString(e));
@@ -1256,6 +1300,22 @@ int bttb_plan_create_from_windows(bttb_plan** out, const bttb_grid* grid, const 
   return plan_create_impl(out, grid, kernel, dtype, device, layer_begin, layer_end, Lx, Ly, nullptr, host_windows);
 }
 
+int bttb_debug_check_guards(bttb_plan* p) {
+  g_err.clear();
+  if (!p) return fail(BTTB_EINVAL, "null plan");
+  if (!guards_on()) return 0;
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard dg(p->device);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(BTTB_ECUDA, "device error before the guard check");
+  int bad = 0;
+  const size_t sbytes = (size_t)p->nzl * p->Hx * p->Ly * p->elem;
+  bad += guard_intact(p->spectra, sbytes) != 0;
+  const DevBuf* bufs[] = {&p->work, &p->hin, &p->hout, &p->cg, &p->cg_hist};
+  for (const DevBuf* b : bufs) bad += b->intact() != 0;
+  for (int i = 0; i < bttb_plan_s::kRing; ++i) bad += (p->ain[i].intact() != 0) + (p->aout[i].intact() != 0);
+  return bad;
+}
+
 int bttb_plan_destroy(bttb_plan* plan) {
   destroy_plan(plan);
   return BTTB_OK;
@@ -1274,7 +1334,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   const size_t in_elems = (size_t)batch * (mode == BTTB_FORWARD ? p->nloc() : p->m());
   const size_t out_elems = (size_t)batch * (mode == BTTB_FORWARD ? p->m() : p->nloc());
   const size_t esz = p->elem / 2;
-  if (where == BTTB_HOST_ASYNC) {
+  if (where == BTTB_HOST_ASYNC || where == BTTB_HOST_ASYNC_UNORDERED) {
     // ring slot i: H2D (s_h2d) -> compute (plan stream) -> D2H (s_d2h); a slot
     // is reused only after its previous compute read ain[i] / its previous D2H
     // read aout[i].  The caller's stream waits for this call's D2H.
@@ -1282,8 +1342,14 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
     p->ring = (p->ring + 1) % bttb_plan_s::kRing;
     int rc;
     if ((rc = p->ain[i].ensure(in_elems * esz)) || (rc = p->aout[i].ensure(out_elems * esz))) return rc;
-    // the input copy is NOT ordered after st's pending work (that would chain
-    // it behind the previous call's output copy): x must be final at call time
+    // BTTB_HOST_ASYNC: the input copy follows the work queued on the caller's
+    // stream (x may be produced there); BTTB_HOST_ASYNC_UNORDERED drops that
+    // edge (it would chain the copy behind the previous call's output copy):
+    // x must be final at call time
+    if (where == BTTB_HOST_ASYNC) {
+      CU(cudaEventRecord(p->ev_in, st));
+      CU(cudaStreamWaitEvent(p->s_h2d, p->ev_in, 0));
+    }
     CU(cudaStreamWaitEvent(p->s_h2d, p->ev_in_free[i], 0));
     CU(cudaMemcpyAsync(p->ain[i].p, x, in_elems * esz, cudaMemcpyHostToDevice, p->s_h2d));
     CU(cudaEventRecord(p->ev_h2d[i], p->s_h2d));
@@ -1309,7 +1375,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
     xd = p->hin.p;
     yd = p->hout.p;
   } else if (where != BTTB_DEVICE_PTR) {
-    return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR, BTTB_HOST_PTR or BTTB_HOST_ASYNC");
+    return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR, BTTB_HOST_PTR, BTTB_HOST_ASYNC or BTTB_HOST_ASYNC_UNORDERED");
   }
   // the work runs on the plan's stream (which carries the L2 window), ordered
   // after everything already queued on the caller's stream and before

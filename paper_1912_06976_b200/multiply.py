@@ -91,10 +91,17 @@ def apply_into(stack, mode, x_ptr, y_ptr, batch=1, stream_ptr=None, host=False):
     """Raw-pointer entry (bench / multi-GPU driver): y <- op(x), no validation copies.
 
     host=False: device pointers; host=True: host pointers, synchronous;
-    host="async": pinned host pointers, returns at once -- x / y are in use
-    until ``stream_ptr`` (default stream if None) is synchronised, and
-    consecutive calls overlap their copies (BTTB_HOST_ASYNC)."""
-    where = _lib.HOST_ASYNC if host == "async" else (_lib.HOST_PTR if host else _lib.DEVICE_PTR)
+    host="async": pinned host pointers, returns at once -- the input copy is
+    ordered after the work already queued on ``stream_ptr`` (default stream if
+    None), x / y are in use until that stream is synchronised
+    (BTTB_HOST_ASYNC); host="async-unordered": the same without the ordering
+    edge (x must be final at call time), so consecutive calls overlap their
+    copies (BTTB_HOST_ASYNC_UNORDERED)."""
+    wheres = {False: _lib.DEVICE_PTR, True: _lib.HOST_PTR, "async": _lib.HOST_ASYNC,
+              "async-unordered": _lib.HOST_ASYNC_UNORDERED}
+    if host not in wheres:
+        raise ValueError(f"host must be one of {sorted(map(str, wheres))}, got {host!r}")
+    where = wheres[host]
     _lib.check(_lib.lib().bttb_apply(stack.handle, _MODES[mode], _lib.ctypes.c_void_p(x_ptr),
                                      _lib.ctypes.c_void_p(y_ptr), int(batch), where,
                                      _lib.ctypes.c_void_p(stream_ptr or 0)))

@@ -30,7 +30,7 @@ layer-range :class:`~paper_1912_06976_b200.transform.TransformStack`.
 import torch
 import torch.distributed as dist
 
-__all__ = ["partition_layers", "DeviceOperator", "ShardedOperator"]
+__all__ = ["partition_layers", "DeviceOperator", "ShardedOperator", "sharded_cgls"]
 
 
 def partition_layers(nz, world):
@@ -205,3 +205,74 @@ class ShardedOperator:
         if self._multi():
             dist.broadcast(d, src=self._root(), group=self.group)
         return self.local.transpose(d, out) if out is not None else self.local.transpose(d)
+
+
+def sharded_cgls(op, d, iters=10, damp=0.0, rtol=1e-13, history=True):
+    """Layer-sharded CGLS (BASELINE configs[4]: "layers sharded" at 1/2/4/8 GPUs).
+
+    ``op`` is a :class:`ShardedOperator`; each rank holds its layer block of
+    the models m, p and s (the same contiguous blocks ``partition_layers``
+    gives the spectrum caches), and the data-space vectors d, r, q are
+    replicated.  Per iteration: the local forward partial G_k p_k, ONE
+    all-reduce of it (the reference's layer sum, multiply.py:42-45, split
+    across ranks -- SPEC.md:316 notes the reduction), the local transpose of
+    the replicated residual (no broadcast needed: every rank holds the same
+    r), and two all-reduces of per-model fp64 scalars (|p|^2 for the damping
+    term, |s|^2).  The recurrences, the fp64 dot products and the freeze rule
+    (alpha = beta = 0 once |s_k| <= rtol |s_0|) are those of the single-GPU
+    loop (``bttb_cgls``) and of the oracle's ``cgls``.
+
+    d: (m,) or (batch, m) tensor (the root's copy is broadcast first).
+    Returns (m_local, hist): this rank's layer block of the models, shaped
+    like d with the last axis n_local, and the residual norms |r_k|,
+    k = 0..iters, as a (batch, iters+1) float64 tensor on d's device (or None).
+    """
+    if int(iters) != iters or iters < 0:
+        raise ValueError(f"iters must be a non-negative integer, got {iters!r}")
+    local, grp = op.local, op.group
+    multi = op._multi()
+
+    def allsum(t):
+        if multi:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=grp)
+        return t
+
+    def dot(a):  # per-model fp64 sum of squares over the last axis
+        return (a.to(torch.float64) ** 2).sum(-1)
+
+    if multi:
+        d = d.contiguous()
+        dist.broadcast(d, src=op._root(), group=grp)
+    dd = float(damp) * float(damp)
+    r = d.clone()
+    s = local.transpose(r)
+    m = torch.zeros_like(s)
+    p = s.clone()
+    gamma = allsum(dot(s))
+    floor = rtol * rtol * gamma
+    hist = [dot(r).sqrt()] if history else None
+    for _ in range(int(iters)):
+        q = allsum(local.forward(p))
+        delta = dot(q)
+        if dd:
+            delta = delta + dd * allsum(dot(p))
+        live = gamma > floor
+        alpha = torch.where((delta > 0) & live, gamma / torch.where(delta > 0, delta, torch.ones_like(delta)),
+                            torch.zeros_like(gamma))
+        a_ = alpha.to(s.dtype).unsqueeze(-1)
+        m = m + a_ * p
+        r = r - a_ * q
+        s = local.transpose(r)
+        if dd:
+            s = s - dd * m
+        gnew = allsum(dot(s))
+        beta = torch.where(live, gnew / torch.where(live, gamma, torch.ones_like(gamma)), torch.zeros_like(gamma))
+        gamma = gnew
+        p = s + beta.to(s.dtype).unsqueeze(-1) * p
+        if history:
+            hist.append(dot(r).sqrt())
+    if history:
+        hist = torch.stack(hist, dim=-1)
+        if hist.dim() == 1:
+            hist = hist.unsqueeze(0)
+    return m, hist

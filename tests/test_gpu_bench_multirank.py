@@ -46,3 +46,14 @@ def test_two_rank_bench_line(reduce):
 def test_two_rank_reference_arm():
     d = _run("--impl", "reference")
     assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_two_rank_layer_sharded_cgls():
+    """--cgls under torchrun shards the depth layers (BASELINE configs[4]):
+    16 of C5's 32 layers per rank, all 64 models on every rank, and the
+    residual still drops like the single-GPU loop's."""
+    d = _run("--config", "C5", "--dtype", "f32", "--cgls", "3")
+    assert d["n_gpus"] == 2 and d["config"]["layers_per_rank"] == 16 and d["config"]["models_per_rank"] == 64
+    assert d["config"]["parallelism"].startswith("layer-shard x2")
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert 0 < d["residual_drop_median"] < 0.9

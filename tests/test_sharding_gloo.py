@@ -115,3 +115,46 @@ def test_two_rank_layer_sharding_matches_unsharded(kind, reduce):
         assert np.array_equal(O.transpose(g, tr, v), xt)
     else:  # same per-layer arithmetic from the broadcast spectrum
         assert O.rel_l2(O.transpose(g, tr, v), xt) <= 1e-14
+
+
+def _cgls_worker(rank, world, port, kind, damp, out):
+    from paper_1912_06976_b200.parallel import sharded_cgls
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = O.ogrid(7, 5, 5, 1, 2, 2, 0, 1.0, 1.5, (0.0, 1.0, 2.5, 4.0, 4.5, 6.0))
+    consts = O.grav_constants() if kind == "gravity" else O.mag_constants(33.0, 47.0, 45000.0)
+    lo, hi = partition_layers(g.nz, world)[rank]
+    op = ShardedOperator(OracleLocal(g, kind, consts, lo, hi))
+    d = np.random.default_rng(21).normal(size=g.m)
+    # only the root's data matters: the others' copies are overwritten by the broadcast
+    dt = torch.from_numpy(d.copy()) if rank == 0 else torch.zeros(g.m, dtype=torch.float64)
+    m_loc, hist = sharded_cgls(op, dt, iters=6, damp=damp)
+    parts = [None] * world
+    dist.all_gather_object(parts, m_loc.numpy())
+    if rank == 0:
+        out["m"] = np.concatenate(parts)
+        out["hist"] = hist.numpy()[0]
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("damp", [0.0, 0.3])
+@pytest.mark.parametrize("kind", ["gravity", "magnetic"])
+def test_two_rank_layer_sharded_cgls_matches_oracle(kind, damp):
+    """Layer-sharded CGLS over 2 gloo ranks (BASELINE configs[4]) equals the
+    oracle's single-process CGLS: models to 1e-12, residual history to 1e-12."""
+    world = 2
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_cgls_worker, args=(world, _free_port(), kind, damp, out), nprocs=world, join=True)
+        m, hist = out["m"], out["hist"]
+    g = O.ogrid(7, 5, 5, 1, 2, 2, 0, 1.0, 1.5, (0.0, 1.0, 2.5, 4.0, 4.5, 6.0))
+    consts = O.grav_constants() if kind == "gravity" else O.mag_constants(33.0, 47.0, 45000.0)
+    fw, tr = O.build_spectra(g, kind, consts)
+    d = np.random.default_rng(21).normal(size=g.m)
+    m_ref, h_ref = O.cgls(g, fw, tr, d, 6, damp=damp)
+    assert O.rel_l2(m_ref, m) <= 1e-12
+    np.testing.assert_allclose(hist, h_ref, rtol=1e-12)
+    if damp == 0.0:
+        assert hist[-1] < hist[0]
