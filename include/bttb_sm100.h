@@ -149,10 +149,13 @@ int bttb_gravity_response(const double* x, int64_t ncx, const double* y, int64_t
 int bttb_magnetic_response(const double* x, int64_t ncx, const double* y, int64_t ncy, const double* r2,
                            double z1, double z2, const double* gc, double* out, int device);
 
-/* FFT length the plan picks for an embedding of n (at most 8192, or -1):
- * the smallest supported length >= n (2^a, a>=3; 2^a*3^b or 2^a*5^b with
- * a>=2, b>=1), except that a power of two within 5% of it is preferred when
- * the library has a compile-time FFT plan for it (e.g. 1999 -> 2048). */
+/* FFT length the plan picks for an embedding of n: the smallest length of
+ * the shared-memory engine's family >= n up to 8192 (2^a, a>=3; 2^a*3^b or
+ * 2^a*5^b with a>=2, b>=1), except that a power of two within 5% of it is
+ * preferred when the library has a compile-time FFT plan for it (e.g.
+ * 1999 -> 2048); above 8192 the smallest 2^a 3^b 5^c >= n (at most 65536),
+ * which plans run on the generic-length path (global-memory radix passes;
+ * no split products).  -1 if n > 65536. */
 int64_t bttb_fft_length(int64_t n);
 
 /* Development check (no reference counterpart): with BTTB_GUARD=1 in the

@@ -23,7 +23,7 @@ UNITS = {
     "entries.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"],
     "spectral.cu": ["-Xptxas", "-v"] if os.environ.get("BTTB_PTXAS_VERBOSE") else [],
     "cgls.cu": [],
-    "fused.cu": ["-Xptxas", "-v"] if os.environ.get("BTTB_PTXAS_VERBOSE") else [],
+    "generic.cu": [],
     "capi.cu": [],
 }
 

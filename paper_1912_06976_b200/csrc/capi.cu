@@ -19,7 +19,7 @@
 #include "bttb_sm100.h"
 #include "cgls.h"
 #include "entries.h"
-#include "fused.h"
+#include "generic.h"
 #include "spectral.h"
 
 using namespace bttb;
@@ -69,7 +69,7 @@ int64_t pick_length(int64_t n) {
   int64_t best = -1;
   for (int64_t L = std::max<int64_t>(n, 8); L <= 8192; ++L)
     if (length_family(L)) { best = L; break; }
-  if (best < 0) return -1;
+  if (best < 0) return generic_length(n);  // above 8192: the generic path (generic.cu)
   static const bool pow2 = !(getenv("BTTB_FFT_POW2") && atoi(getenv("BTTB_FFT_POW2")) == 0);
   int64_t p2 = 8;
   while (p2 < n) p2 *= 2;
@@ -315,26 +315,6 @@ size_t chunk_budget() {
 
 size_t round_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
 
-// column stages: L2 prefetch distance in layers for the streamed Y / S columns
-// (BTTB_L2_AHEAD; 0 or 1 = off)
-int l2_ahead() {
-  static const int v = getenv("BTTB_L2_AHEAD") ? atoi(getenv("BTTB_L2_AHEAD")) : 0;
-  return v;
-}
-
-// overlap the row pass of chunk c+1 with the column stage of chunk c on two
-// streams (double-buffered chunk workspace); opt-in with BTTB_PIPELINE=1
-bool pipelined() {
-  static const bool on = getenv("BTTB_PIPELINE") && atoi(getenv("BTTB_PIPELINE")) != 0;  // measured slower: 8.66 vs 7.16 ms
-  return on;
-}
-
-// transpose intermediate layout: row-major [q][kx] (BTTB_TRA_ROWMAJOR=1) or [kx][q]
-bool tra_rowmajor() {
-  static const bool rm = getenv("BTTB_TRA_ROWMAJOR") && atoi(getenv("BTTB_TRA_ROWMAJOR")) != 0;
-  return rm;
-}
-
 }  // namespace
 
 struct bttb_plan_s {
@@ -348,11 +328,14 @@ struct bttb_plan_s {
   FFTPlanHost fx, fy;
   size_t elem = 16;
   void* spectra = nullptr;
-  bool fused = false;  // fused whole-stack kernels (fused.cu); spectra stored ky-split
+  // generic-length path (generic.cu): lengths outside the shared-memory
+  // engine's family (above 8192), or every plan under BTTB_GENERIC=1
+  bool generic = false;
+  GenericCtx gen;
+  double2* gen_tw[2] = {nullptr, nullptr};
   DevBuf work, hin, hout;
   DevBuf cg, cg_hist;  // CGLS driver workspace and residual history (bttb_cgls)
-  cudaStream_t stream = nullptr;   // internal stream carrying the L2 persisting window (row passes)
-  cudaStream_t stream2 = nullptr;  // second stream: column stages, overlapped with the next chunk's row pass
+  cudaStream_t stream = nullptr;   // internal stream the products run on
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // BTTB_HOST_ASYNC: copy streams and a ring of device staging slots, so one
   // call's device-to-host copy overlaps the next calls' host-to-device copies
@@ -364,11 +347,7 @@ struct bttb_plan_s {
   cudaEvent_t ev_h2d[kRing] = {}, ev_in_free[kRing] = {}, ev_out_ready[kRing] = {}, ev_out_free[kRing] = {};
   cudaEvent_t ev_call = nullptr;
   int ring = 0;
-  cudaEvent_t ev_row[2] = {nullptr, nullptr}, ev_col[2] = {nullptr, nullptr}, ev_aux = nullptr;
-  void* window_base = nullptr;
-  size_t window_bytes = 0;
   int64_t last_K = 0, last_G = 0, last_launches = 0;
-  int* pipe_err_host = nullptr;  // pinned copy of the fused pipeline's deadlock-guard flag
   std::mutex mu;
 
   int64_t n_r() const { return nx * ny; }
@@ -489,7 +468,8 @@ int build_spectra(bttb_plan_s* p, const double* host_windows = nullptr) {
   }
   cudaStream_t st = 0;
   const EmbedArgs ea = embed_args(p);
-  const FFTDesc<double> dx = p->fx.desc<double>(), dy = p->fy.desc<double>();
+  const FFTDesc<double> dx = p->generic ? FFTDesc<double>{} : p->fx.desc<double>();
+  const FFTDesc<double> dy = p->generic ? FFTDesc<double>{} : p->fy.desc<double>();
   const double scale = 1.0 / ((double)p->Lx * (double)p->Ly);
   for (int64_t r = 0; r < p->nzl && !rc; ++r) {
     const int64_t g = p->l0 + r;
@@ -506,6 +486,13 @@ int build_spectra(bttb_plan_s* p, const double* host_windows = nullptr) {
                        p->z[g], p->z[g + 1], gc5(p), (int*)s.flag.p, (double*)emb.p, st);
     }
     if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "embed: %s", cudaGetErrorString(e)); break; }
+    if (p->generic) {
+      void* sr = static_cast<char*>(p->spectra) + (size_t)r * p->Hx * p->Ly * p->elem;
+      e = p->dtype == BTTB_F64 ? generic_build_layer<double>(p->gen, (const double*)emb.p, sr, st)
+                               : generic_build_layer<float>(p->gen, (const double*)emb.p, sr, st);
+      if (e != cudaSuccess) { rc = fail(BTTB_ECUDA, "generic spectrum build: %s", cudaGetErrorString(e)); break; }
+      continue;
+    }
     RowR2CArgs ra{};
     ra.in = emb.p;
     ra.in_bstride = 0;
@@ -544,362 +531,59 @@ int build_spectra(bttb_plan_s* p, const double* host_windows = nullptr) {
   return rc;
 }
 
-// Persisting L2 window over the chunk workspace (device-wide persisting
-// carve-out raised to cover it, capped by the hardware maximum).
-int set_l2_window(bttb_plan_s* p, void* base, size_t bytes) {
-  // opt-in (BTTB_L2_WINDOW=1): with whole-stack chunks the persisting window
-  // only pins a fraction of the intermediate and measured slower
-  if (!(getenv("BTTB_L2_WINDOW") && atoi(getenv("BTTB_L2_WINDOW")) != 0)) return BTTB_OK;
-  if (base == p->window_base && bytes == p->window_bytes) return BTTB_OK;
-  int maxwin = 0, maxpersist = 0;
-  CU(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
-  CU(cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, p->device));
-  if (maxwin <= 0 || maxpersist <= 0) return BTTB_OK;
-  size_t cur = 0;
-  CU(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-  const size_t want = std::min(bytes, (size_t)maxpersist);
-  if (cur < want) CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-  CU(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-  cudaStreamAttrValue v{};
-  v.accessPolicyWindow.base_ptr = base;
-  v.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)maxwin);
-  v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)cur / (double)v.accessPolicyWindow.num_bytes);
-  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  CU(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-  CU(cudaStreamSetAttribute(p->stream2, cudaStreamAttributeAccessPolicyWindow, &v));
-  p->window_base = base;
-  p->window_bytes = bytes;
-  return BTTB_OK;
-}
-
-// Fused layer pipeline (pipeline.cuh), square FFT lengths with a pipeline
-// plan: per vector, forward = pipeline kernel + row C2R of the stations;
-// transpose = row R2C of the data + pipeline kernel.  Workspace: the ring of
-// two layer intermediates, the station half spectrum W, the counters.
-template <class T>
-int run_pipe(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st) {
-  using V = cplx<T>;
-  const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
-  const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
-                nloc = p->nloc();
-  if (p->pipe_err_host && *p->pipe_err_host)
-    return fail(BTTB_ECUDA, "fused pipeline deadlock guard tripped in an earlier apply");
-  if (!p->pipe_err_host) CU(cudaMallocHost(&p->pipe_err_host, sizeof(int)));
-  static const int nb_env = getenv("BTTB_PIPE_NB") ? atoi(getenv("BTTB_PIPE_NB")) : 3;
-  const int NB = std::max(2, nb_env);  // ring slots (>= 2: see pipeline.cuh)
-  const size_t ring = round_up((size_t)NB * Hx * ny * sizeof(V), 4096);
-  const size_t wbytes = round_up((size_t)Hx * sy * sizeof(V), 4096);
-  const int ncnt = pipe_counter_ints((int)p->nzl);
-  const size_t cbytes = (size_t)ncnt * sizeof(int);
-  // BTTB_PIPE_STATS=1: per-team cycle accounting printed to stderr (development aid)
-  static const bool stats_on = getenv("BTTB_PIPE_STATS") && atoi(getenv("BTTB_PIPE_STATS")) != 0;
-  const size_t sbytes = stats_on ? (size_t)8 * pipe_grid() * pipe_teams() * sizeof(long long) : 0;
-  int rc;
-  if ((rc = p->work.ensure(ring + wbytes + round_up(cbytes, 4096) + sbytes))) return rc;
-  char* base = static_cast<char*>(p->work.p);
-  V* Wb = reinterpret_cast<V*>(base + ring);
-  int* cnt = reinterpret_cast<int*>(base + ring + wbytes);
-  long long* stats = stats_on ? reinterpret_cast<long long*>(base + ring + wbytes + round_up(cbytes, 4096)) : nullptr;
-  CU(cudaMemsetAsync(cnt, 0, cbytes, st));  // counters and the err flag (last int)
-  PipeArgs a{};
-  a.S = p->spectra;
-  a.s_rstride = (long long)Hx * p->Ly;
-  a.lds = (int)p->Ly;
-  a.ring = base;
-  a.ring_sstride = (long long)Hx * ny;
-  a.nb = NB;
-  a.sync = cnt;
-  a.nz = (int)p->nzl;
-  a.nx = (int)nx;
-  a.ny = (int)ny;
-  a.sy = (int)sy;
-  a.Hx = (int)Hx;
-  a.n_r = n_r;
-  a.stats = stats;
-  p->last_K = p->nzl;
-  p->last_G = 1;
-  int64_t launches = 0;
-  for (int64_t b = 0; b < batch; ++b) {
-    if (b > 0) CU(cudaMemsetAsync(cnt, 0, cbytes - sizeof(int), st));
-    if (mode == BTTB_FORWARD) {
-      a.in = static_cast<const T*>(x) + b * nloc;
-      a.out = Wb;
-      CU(launch_pipe<T>(0, a, dy, st));
-      RowC2RArgs oa{};
-      oa.in = Wb;
-      oa.in_sstride = (long long)Hx * sy;
-      oa.ld_in = (int)sy;
-      oa.nrows = (int)sy;
-      oa.Hx = (int)Hx;
-      oa.nslabs = 1;
-      oa.out = static_cast<T*>(y) + b * m;
-      oa.out_bstride = m;
-      oa.out_sstride = 0;
-      oa.spb = 1;
-      oa.ld_out = (int)sx;
-      oa.nout = (int)sx;
-      oa.tw_816 = tw816<T>(p->fx);
-      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
-    } else {
-      RowR2CArgs ra{};
-      ra.in = static_cast<const T*>(x) + b * m;
-      ra.in_bstride = m;
-      ra.in_sstride = 0;
-      ra.spb = 1;
-      ra.ld_in = (int)sx;
-      ra.nrows = (int)sy;
-      ra.nvalid = (int)sx;
-      ra.nslabs = 1;
-      ra.out = Wb;
-      ra.out_sstride = (long long)Hx * sy;
-      ra.ld_out = (int)sy;
-      ra.Hx = (int)Hx;
-      CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
-      a.in = Wb;
-      a.out = static_cast<T*>(y) + b * nloc;
-      CU(launch_pipe<T>(1, a, dy, st));
-    }
-    launches += 2;
-  }
-  CU(cudaMemcpyAsync(p->pipe_err_host, cnt + ncnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-  if (stats_on) {  // last vector's accounting
-    const int n = pipe_grid() * pipe_teams();
-    std::vector<long long> hs((size_t)8 * n);
-    CU(cudaMemcpyAsync(hs.data(), stats, sbytes, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    {
-      int nzero = 0;
-      std::string ids;
-      for (int i = 0; i < n; ++i)
-        if (hs[8 * i + 6] == 0) {
-          if (nzero++ < 12) ids += " " + std::to_string(i);
-        }
-      if (nzero) fprintf(stderr, "[pipe] %d of %d teams wrote no stats:%s\n", nzero, n, ids.c_str());
-    }
-    double acc[6] = {0, 0, 0, 0, 0, 0}, mx[6] = {0, 0, 0, 0, 0, 0};
-    long long g0 = hs[6], g1 = hs[7];
-    for (int i = 0; i < n; ++i) {
-      for (int j = 0; j < 6; ++j) {
-        acc[j] += (double)hs[8 * i + j];
-        mx[j] = std::max(mx[j], (double)hs[8 * i + j]);
-      }
-      g0 = std::min(g0, hs[8 * i + 6]);
-      g1 = std::max(g1, hs[8 * i + 7]);
-    }
-    // start / end offsets (us) of the teams relative to the first start
-    std::vector<double> so(n), eo(n);
-    for (int i = 0; i < n; ++i) {
-      so[i] = (hs[8 * i + 6] - g0) * 1e-3;
-      eo[i] = (hs[8 * i + 7] - g0) * 1e-3;
-    }
-    std::sort(so.begin(), so.end());
-    std::sort(eo.begin(), eo.end());
-    fprintf(stderr,
-            "[pipe %s] span %.1f us; start offsets med/max %.1f/%.1f us; ends min/med/max %.1f/%.1f/%.1f us; per team "
-            "mean/max cycles: total %.0f/%.0f, wait %.0f/%.0f, rows %.0f/%.0f (%.1f items), cols %.0f/%.0f (%.1f items)\n",
-            mode == BTTB_FORWARD ? "fwd" : "tra", (g1 - g0) * 1e-3, so[n / 2], so[n - 1], eo[0], eo[n / 2], eo[n - 1],
-            acc[5] / n, mx[5], acc[0] / n, mx[0], acc[1] / n, mx[1], acc[3] / n, acc[2] / n, mx[2], acc[4] / n);
-  }
-  p->last_launches = launches;
-  return BTTB_OK;
-}
-
-// the fused pipeline runs square lengths >= BTTB_PIPE_MIN_L (default 1024;
-// smaller stacks fit L2 and batch better in the staged path); BTTB_PIPE=0 off
-bool use_pipe(const bttb_plan_s* p) {
-  static const int64_t min_l = getenv("BTTB_PIPE_MIN_L") ? atoll(getenv("BTTB_PIPE_MIN_L")) : 1024;
-  if (p->Lx != p->Ly || p->Lx < min_l) return false;
-  return p->dtype == BTTB_F64 ? pipe_supported<double>((int)p->Lx, (int)p->Hx)
-                              : pipe_supported<float>((int)p->Lx, (int)p->Hx);
-}
-
-// Fused whole-stack kernels (fused.cu): per vector, forward = fused kernel
-// (row transforms + column stages of every layer, L2 ring, TMEM accumulators)
-// writing the station half spectrum W[kx][j < sy], then the row C2R of the
-// stations; transpose = row R2C of the data into W, then the fused kernel.
-// The split stages meet at W exactly as in the staged path (run_apply).
-template <class T>
-int run_fused(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st, int stage) {
-  using V = cplx<T>;
-  const bool rows_in = stage != BTTB_STAGE_FROM_SPECTRUM, rows_out = stage != BTTB_STAGE_TO_SPECTRUM;
-  const FFTDesc<T> dx = p->fx.desc<T>();
-  const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, m = p->m(), nloc = p->nloc();
-  static const int look_env = getenv("BTTB_FUSED_AHEAD") ? atoi(getenv("BTTB_FUSED_AHEAD")) : 2;
-  const int D = std::max(1, look_env), NB = D + 1;
-  const int64_t ring_ld = (ny + 1) & ~int64_t(1);
-  const size_t ring = round_up((size_t)NB * Hx * ring_ld * sizeof(V), 4096);
-  const size_t wbytes = round_up((size_t)Hx * sy * sizeof(V), 4096);
-  const int ncnt = fused_counter_ints((int)p->nzl);
-  const size_t cbytes = round_up((size_t)ncnt * sizeof(int), 4096);
-  int rc;
-  // BTTB_FUSED_STATS=1: per-warp cycle accounting of the last vector, printed to stderr (development aid)
-  static const bool stats_on = getenv("BTTB_FUSED_STATS") && atoi(getenv("BTTB_FUSED_STATS")) != 0;
-  const int nwarps = fused_grid() * fused_warps(std::is_same<T, double>::value);
-  const size_t sbytes = stats_on ? (size_t)nwarps * FZ_NSTAT * sizeof(long long) : 0;
-  if ((rc = p->work.ensure(ring + wbytes + cbytes + sbytes))) return rc;
-  char* base = static_cast<char*>(p->work.p);
-  V* Wb = reinterpret_cast<V*>(base + ring);
-  int* cnt = reinterpret_cast<int*>(base + ring + wbytes);
-  long long* stats = stats_on ? reinterpret_cast<long long*>(base + ring + wbytes + cbytes) : nullptr;
-  if (!p->pipe_err_host) CU(cudaMallocHost(&p->pipe_err_host, sizeof(int)));
-  if (*p->pipe_err_host) return fail(BTTB_ECUDA, "fused kernel deadlock guard tripped in an earlier apply");
-  FusedArgs a{};
-  a.S = p->spectra;
-  a.s_rstride = (long long)Hx * p->Ly;
-  a.ring = base;
-  a.ring_sstride = (long long)Hx * ring_ld;
-  a.ring_ld = (int)ring_ld;
-  a.nb = NB;
-  a.sync = cnt;
-  a.tw = std::is_same<T, double>::value ? (const void*)p->fy.tw64 : (const void*)p->fy.tw32;
-  a.nz = (int)p->nzl;
-  a.nx = (int)nx;
-  a.ny = (int)ny;
-  a.sx = (int)sx;
-  a.sy = (int)sy;
-  a.Hx = (int)Hx;
-  a.npairs = (int)((ny + 1) / 2);
-  a.n_r = p->n_r();
-  a.lookahead = D;
-  a.stats = stats;
-  p->last_K = p->nzl;
-  p->last_G = 1;
-  int64_t launches = 0;
-  for (int64_t b = 0; b < batch; ++b) {
-    if (mode == BTTB_FORWARD) {
-      V* Wg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b * Hx * sy
-              : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b * Hx * sy
-                                                  : Wb;
-      if (rows_in) {
-        CU(cudaMemsetAsync(cnt, 0, (size_t)ncnt * sizeof(int), st));
-        a.in = static_cast<const T*>(x) + b * nloc;
-        a.out = Wg;
-        CU(launch_fused<T>(0, a, st));
-        CU(cudaMemcpyAsync(p->pipe_err_host, cnt + ncnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-        launches += 1;
-      }
-      if (rows_out) {
-        RowC2RArgs oa{};
-        oa.in = Wg;
-        oa.in_sstride = (long long)Hx * sy;
-        oa.ld_in = (int)sy;
-        oa.nrows = (int)sy;
-        oa.Hx = (int)Hx;
-        oa.nslabs = 1;
-        oa.out = static_cast<T*>(y) + b * m;
-        oa.out_bstride = m;
-        oa.out_sstride = 0;
-        oa.spb = 1;
-        oa.ld_out = (int)sx;
-        oa.nout = (int)sx;
-        oa.tw_816 = tw816<T>(p->fx);
-        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
-        launches += 1;
-      }
-    } else {
-      V* Dg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b * Hx * sy
-              : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b * Hx * sy
-                                                  : Wb;
-      if (rows_in) {
-        RowR2CArgs ra{};
-        ra.in = static_cast<const T*>(x) + b * m;
-        ra.in_bstride = m;
-        ra.in_sstride = 0;
-        ra.spb = 1;
-        ra.ld_in = (int)sx;
-        ra.nrows = (int)sy;
-        ra.nvalid = (int)sx;
-        ra.nslabs = 1;
-        ra.out = Dg;
-        ra.out_sstride = (long long)Hx * sy;
-        ra.ld_out = (int)sy;
-        ra.Hx = (int)Hx;
-        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
-        launches += 1;
-      }
-      if (rows_out) {
-        CU(cudaMemsetAsync(cnt, 0, (size_t)ncnt * sizeof(int), st));
-        a.in = Dg;
-        a.out = static_cast<T*>(y) + b * nloc;
-        CU(launch_fused<T>(1, a, st));
-        CU(cudaMemcpyAsync(p->pipe_err_host, cnt + ncnt - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-        launches += 1;
-      }
-    }
-  }
-  p->last_launches = launches;
-  if (stats_on) {
-    std::vector<long long> hs((size_t)nwarps * FZ_NSTAT);
-    CU(cudaMemcpyAsync(hs.data(), stats, sbytes, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    double mean[FZ_NSTAT] = {0}, mx[FZ_NSTAT] = {0};
-    for (int i = 0; i < nwarps; ++i)
-      for (int j = 0; j < FZ_NSTAT; ++j) {
-        mean[j] += (double)hs[(size_t)i * FZ_NSTAT + j] / nwarps;
-        mx[j] = std::max(mx[j], (double)hs[(size_t)i * FZ_NSTAT + j]);
-      }
-    fprintf(stderr,
-            "[fused %s] per warp mean/max kcycles: total %.0f/%.0f wait %.0f/%.0f grab %.0f/%.0f rows %.0f/%.0f "
-            "(%.2f/%.0f items) cols %.0f/%.0f (%.2f/%.0f items) pro/epi %.0f/%.0f\n",
-            mode == BTTB_FORWARD ? "fwd" : "tra", mean[5] / 1e3, mx[5] / 1e3, mean[0] / 1e3, mx[0] / 1e3,
-            mean[1] / 1e3, mx[1] / 1e3, mean[2] / 1e3, mx[2] / 1e3, mean[6], mx[6], mean[3] / 1e3, mx[3] / 1e3,
-            mean[7], mx[7], mean[4] / 1e3, mx[4] / 1e3);
-  }
-  return BTTB_OK;
-}
-
-// the fused kernels run plans whose geometry they support (fused_supported)
-// when BTTB_FUSED=1 (opt-in while they are slower than the staged kernels)
-bool use_fused(const bttb_plan_s* p) {
-  static const bool on = getenv("BTTB_FUSED") && atoi(getenv("BTTB_FUSED")) != 0;
-  return on && fused_supported(p->Lx, p->Ly, p->nx, p->ny, p->sx, p->sy);
-}
-
 // stage: BTTB_STAGE_ALL runs the whole product; the split stages meet at the
 // station half spectrum W[b][kx][j < sy] (x frequency, y space: Hx x sy complex
 // per item) -- forward: TO_SPECTRUM = row R2C + column stage (the plan's layers'
 // partial W, column-inverse-transformed), FROM_SPECTRUM = row C2R of a (summed)
 // W; transpose: TO_SPECTRUM = row R2C of the data, FROM_SPECTRUM = column stage +
 // row C2R into the plan's layers.  x / y are then W where the stage says so.
+// generic-length path (generic.cu): whole products only, one vector at a time
+template <class T>
+int run_generic(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st, int stage) {
+  if (stage != BTTB_STAGE_ALL)
+    return fail(BTTB_EINVAL, "split products are not available for the generic-length plan (FFT lengths %lld x %lld)",
+                (long long)p->Lx, (long long)p->Ly);
+  const int64_t nloc = p->nloc(), m = p->m();
+  for (int64_t b = 0; b < batch; ++b) {
+    if (mode == BTTB_FORWARD)
+      CU((generic_forward<T>(p->gen, p->spectra, p->nzl, static_cast<const T*>(x) + b * nloc, (int)p->nx, (int)p->ny,
+                             static_cast<T*>(y) + b * m, (int)p->sx, (int)p->sy, st)));
+    else
+      CU((generic_transpose<T>(p->gen, p->spectra, p->nzl, static_cast<const T*>(x) + b * m, (int)p->sx,
+                               (int)p->sy, static_cast<T*>(y) + b * nloc, (int)p->nx, (int)p->ny, st)));
+  }
+  p->last_K = p->nzl;
+  p->last_G = 1;
+  p->last_launches = -1;  // many small pass kernels; not counted
+  return BTTB_OK;
+}
+
 template <class T>
 int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st,
               int stage = BTTB_STAGE_ALL) {
-  if (p->fused) return run_fused<T>(p, mode, x, y, batch, st, stage);
-  if (stage == BTTB_STAGE_ALL && use_pipe(p)) return run_pipe<T>(p, mode, x, y, batch, st);
+  if (p->generic) return run_generic<T>(p, mode, x, y, batch, st, stage);
   const bool rows_in = stage != BTTB_STAGE_FROM_SPECTRUM, rows_out = stage != BTTB_STAGE_TO_SPECTRUM;
   using V = cplx<T>;
   const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
   const int64_t Hx = p->Hx, nx = p->nx, ny = p->ny, sx = p->sx, sy = p->sy, n_r = p->n_r(), m = p->m(),
                 nloc = p->nloc();
-  const int64_t Hxp = (Hx + 1) & ~int64_t(1);  // row length of the row-major transpose intermediate
-  const size_t slab = (size_t)Hxp * ny * sizeof(V);
+  const size_t slab = (size_t)Hx * ny * sizeof(V);
   const size_t budget = chunk_budget();
   int64_t K = std::max<int64_t>(1, std::min<int64_t>(p->nzl, (int64_t)(budget / slab)));
   int64_t G = 1;
   if (K == p->nzl) G = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(budget / (slab * p->nzl))));
   int rc;
-  // workspace: two chunk intermediates Y[0..1] (row-pass output / transposed
-  // column output; double-buffered so chunk c+1's row pass overlaps chunk c's
-  // column stage) then the accumulator / data half-spectrum W
-  const bool pipe = pipelined();
-  const int nbuf = pipe ? 2 : 1;
+  // workspace: the chunk intermediate Y (row-pass output / transposed column
+  // output) then the accumulator / data half-spectrum W
   const size_t ybytes = round_up(slab * K * G, 4096), wbytes = round_up((size_t)Hx * sy * sizeof(V) * G, 4096);
-  if ((rc = p->work.ensure(nbuf * ybytes + wbytes))) return rc;
-  if ((rc = set_l2_window(p, p->work.p, nbuf * ybytes + wbytes))) return rc;
+  if ((rc = p->work.ensure(ybytes + wbytes))) return rc;
   p->last_K = K;
   p->last_G = G;
   int64_t launches = 0;
-  V* Ybuf[2] = {static_cast<V*>(p->work.p), reinterpret_cast<V*>(static_cast<char*>(p->work.p) + (pipe ? ybytes : 0))};
-  V* Wb = reinterpret_cast<V*>(static_cast<char*>(p->work.p) + nbuf * ybytes);
+  V* Yb = static_cast<V*>(p->work.p);
+  V* Wb = reinterpret_cast<V*>(static_cast<char*>(p->work.p) + ybytes);
   const V* S = static_cast<const V*>(p->spectra);
   const long long s_rstride = (long long)Hx * p->Ly;
-  cudaStream_t sa = st, sb = pipe ? p->stream2 : st;  // sa: row passes, sb: column stages
-  if (pipe) {
-    CU(cudaEventRecord(p->ev_aux, sa));  // sb starts after everything already ordered on sa
-    CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
-  }
-  int chunk = 0;
   for (int64_t b0 = 0; b0 < batch; b0 += G) {
     const int gb = (int)std::min<int64_t>(G, batch - b0);
     if (mode == BTTB_FORWARD) {
@@ -908,11 +592,8 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       V* Wg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b0 * Hx * sy
               : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b0 * Hx * sy
                                                   : Wb;
-      for (int64_t r0 = 0; rows_in && r0 < p->nzl; r0 += K, ++chunk) {
+      for (int64_t r0 = 0; rows_in && r0 < p->nzl; r0 += K) {
         const int k = (int)std::min<int64_t>(K, p->nzl - r0);
-        const int bi = chunk % nbuf;
-        V* Yb = Ybuf[bi];
-        if (pipe) CU(cudaStreamWaitEvent(sa, p->ev_col[bi], 0));  // column stage of chunk-2 done with Yb
         RowR2CArgs ra{};
         ra.in = xin + r0 * n_r;
         ra.in_bstride = nloc;
@@ -926,11 +607,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ra.out_sstride = (long long)Hx * ny;
         ra.ld_out = (int)ny;
         ra.Hx = (int)Hx;
-        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), sa));
-        if (pipe) {
-          CU(cudaEventRecord(p->ev_row[bi], sa));
-          CU(cudaStreamWaitEvent(sb, p->ev_row[bi], 0));
-        }
+        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
         ColFwdArgs ca{};
         ca.Y = Yb;
         ca.y_bstride = (long long)k * Hx * ny;
@@ -948,14 +625,8 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.accumulate = r0 > 0;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
-        ca.ahead = l2_ahead();
-        CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), sb));
-        if (pipe) CU(cudaEventRecord(p->ev_col[bi], sb));
+        CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), st));
         launches += 2;
-      }
-      if (pipe) {
-        CU(cudaEventRecord(p->ev_aux, sb));
-        CU(cudaStreamWaitEvent(sa, p->ev_aux, 0));
       }
       if (!rows_out) continue;
       RowC2RArgs oa{};
@@ -972,43 +643,32 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       oa.ld_out = (int)sx;
       oa.nout = (int)sx;
       oa.tw_816 = tw816<T>(p->fx);
-      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), sa));
+      CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
       launches += 1;
-      if (pipe) {  // the next batch group's column stages must not overwrite W early
-        CU(cudaEventRecord(p->ev_aux, sa));
-        CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
-      }
     } else {
       V* Dg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b0 * Hx * sy
               : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b0 * Hx * sy
                                                   : Wb;
       if (rows_in) {
-      RowR2CArgs ra{};
-      ra.in = static_cast<const T*>(x) + b0 * m;
-      ra.in_bstride = m;
-      ra.in_sstride = 0;
-      ra.spb = 1;
-      ra.ld_in = (int)sx;
-      ra.nrows = (int)sy;
-      ra.nvalid = (int)sx;
-      ra.nslabs = gb;
-      ra.out = Dg;
-      ra.out_sstride = (long long)Hx * sy;
-      ra.ld_out = (int)sy;
-      ra.Hx = (int)Hx;
-      CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), sa));
-      launches += 1;
-      if (pipe) {
-        CU(cudaEventRecord(p->ev_aux, sa));
-        CU(cudaStreamWaitEvent(sb, p->ev_aux, 0));
-      }
+        RowR2CArgs ra{};
+        ra.in = static_cast<const T*>(x) + b0 * m;
+        ra.in_bstride = m;
+        ra.in_sstride = 0;
+        ra.spb = 1;
+        ra.ld_in = (int)sx;
+        ra.nrows = (int)sy;
+        ra.nvalid = (int)sx;
+        ra.nslabs = gb;
+        ra.out = Dg;
+        ra.out_sstride = (long long)Hx * sy;
+        ra.ld_out = (int)sy;
+        ra.Hx = (int)Hx;
+        CU(launch_row_r2c<T>(ra, dx, p->fx.template E<T>(), st));
+        launches += 1;
       }
       T* yout = static_cast<T*>(y) + b0 * nloc;
-      for (int64_t r0 = 0; rows_out && r0 < p->nzl; r0 += K, ++chunk) {
+      for (int64_t r0 = 0; rows_out && r0 < p->nzl; r0 += K) {
         const int k = (int)std::min<int64_t>(K, p->nzl - r0);
-        const int bi = chunk % nbuf;
-        V* Yb = Ybuf[bi];
-        if (pipe) CU(cudaStreamWaitEvent(sb, p->ev_row[bi], 0));  // row pass of chunk-2 done reading Yb
         ColTraArgs ca{};
         ca.D = Dg;
         ca.d_bstride = (long long)Hx * sy;
@@ -1019,23 +679,17 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         ca.lds = (int)p->Ly;
         ca.K = k;
         ca.W = Yb;
-        ca.w_bstride = (long long)k * Hxp * ny;
-        ca.w_rstride = (long long)Hxp * ny;
-        ca.rowmajor = tra_rowmajor() ? 1 : 0;
-        ca.ldw = ca.rowmajor ? (int)Hxp : (int)ny;  // row-major [q][kx]: the C2R pass reads contiguous rows
+        ca.w_bstride = (long long)k * Hx * ny;
+        ca.w_rstride = (long long)Hx * ny;
+        ca.ldw = (int)ny;
         ca.nout = (int)ny;
         ca.Hx = (int)Hx;
         ca.nbatch = gb;
-        ca.ahead = l2_ahead();
-        CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), sb));
-        if (pipe) {
-          CU(cudaEventRecord(p->ev_col[bi], sb));
-          CU(cudaStreamWaitEvent(sa, p->ev_col[bi], 0));
-        }
+        CU(launch_col_tra<T>(ca, dy, p->fy.template E<T>(), st));
         RowC2RArgs oa{};
         oa.in = Yb;
-        oa.in_sstride = (long long)Hxp * ny;
-        oa.ld_in = ca.rowmajor ? (int)Hxp : (int)ny;
+        oa.in_sstride = (long long)Hx * ny;
+        oa.ld_in = (int)ny;
         oa.nrows = (int)ny;
         oa.Hx = (int)Hx;
         oa.nslabs = gb * k;
@@ -1045,15 +699,9 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         oa.spb = k;
         oa.ld_out = (int)nx;
         oa.nout = (int)nx;
-        oa.rowmajor = ca.rowmajor;
         oa.tw_816 = tw816<T>(p->fx);
-        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), sa));
-        if (pipe) CU(cudaEventRecord(p->ev_row[bi], sa));
+        CU(launch_row_c2r<T>(oa, dx, p->fx.template E<T>(), st));
         launches += 2;
-      }
-      if (pipe) {  // W (the data half-spectrum) is rewritten by the next batch group's row pass on sa
-        CU(cudaEventRecord(p->ev_aux, sb));
-        CU(cudaStreamWaitEvent(sa, p->ev_aux, 0));
       }
     }
   }
@@ -1061,23 +709,28 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
   return BTTB_OK;
 }
 
+void generic_release(bttb_plan_s* p) {
+  for (double2*& t : p->gen_tw) {
+    if (t) cudaFree(t);
+    t = nullptr;
+  }
+  for (double2** b : {&p->gen.A, &p->gen.B, &p->gen.C}) {
+    guard_free(*b);
+    *b = nullptr;
+  }
+}
+
 void destroy_plan(bttb_plan_s* p) {
   if (!p) return;
   DeviceGuard g(p->device);
   if (p->spectra) guard_free(p->spectra);
-  if (p->pipe_err_host) cudaFreeHost(p->pipe_err_host);
+  generic_release(p);
   p->fx.release();
   p->fy.release();
   p->work.release();
   p->cg.release();
   p->cg_hist.release();
   if (p->stream) cudaStreamDestroy(p->stream);
-  if (p->stream2) cudaStreamDestroy(p->stream2);
-  for (int i = 0; i < 2; ++i) {
-    if (p->ev_row[i]) cudaEventDestroy(p->ev_row[i]);
-    if (p->ev_col[i]) cudaEventDestroy(p->ev_col[i]);
-  }
-  if (p->ev_aux) cudaEventDestroy(p->ev_aux);
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
   if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
   for (int i = 0; i < bttb_plan_s::kRing; ++i) {
@@ -1169,6 +822,35 @@ const char* bttb_version(void) { return "bttb_sm100 0.1.0 (sm_100a)"; }
 
 int64_t bttb_fft_length(int64_t n) { return pick_length(n); }
 
+// generic path setup: exact twiddle tables exp(-2 pi i t / L) (extended
+// precision, rounded once) and the three work grids
+static int generic_init(bttb_plan_s* p) {
+  const int64_t Ls[2] = {p->Lx, p->Ly};
+  for (int a = 0; a < 2; ++a) {
+    std::vector<double2> h(Ls[a]);
+    for (int64_t m = 0; m < Ls[a]; ++m) {
+      const long double ang = 2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)Ls[a];
+      h[m] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+    }
+    CU(cudaMalloc(&p->gen_tw[a], sizeof(double2) * Ls[a]));
+    CU(cudaMemcpy(p->gen_tw[a], h.data(), sizeof(double2) * Ls[a], cudaMemcpyHostToDevice));
+  }
+  GenericCtx& g = p->gen;
+  g.Lx = (int)p->Lx;
+  g.Ly = (int)p->Ly;
+  g.Hx = (int)p->Hx;
+  if (g.fx.init(g.Lx, p->gen_tw[0]) || g.fy.init(g.Ly, p->gen_tw[1]))
+    return fail(BTTB_EINVAL, "no radix plan for lengths (%d, %d)", g.Lx, g.Ly);
+  const size_t n = (size_t)p->Lx * p->Ly * sizeof(double2);
+  double2** bufs[3] = {&g.A, &g.B, &g.C};
+  for (double2** b : bufs)
+    if (guard_alloc(reinterpret_cast<void**>(b), n)) {
+      *b = nullptr;
+      return fail(BTTB_ENOMEM, "cannot allocate %zu bytes of generic-path work grid", n);
+    }
+  return BTTB_OK;
+}
+
 static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_kernel* kernel, int dtype,
                             int device, int64_t layer_begin, int64_t layer_end, int64_t Lx, int64_t Ly,
                             const void* host_spectra, const double* host_windows = nullptr) {
@@ -1217,16 +899,23 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
   p->Lx = Lx > 0 ? Lx : pick_length(p->mx);
   p->Ly = Ly > 0 ? Ly : pick_length(p->my);
   int rc = BTTB_OK;
-  if (p->Lx < p->mx || p->Ly < p->my || !length_family(p->Lx) || !length_family(p->Ly)) {
-    rc = fail(BTTB_EINVAL, "FFT lengths (%lld, %lld) unsupported for embedding (%lld, %lld)", (long long)p->Lx,
-              (long long)p->Ly, (long long)p->mx, (long long)p->my);
+  // the shared-memory engine covers its length family up to 8192; anything
+  // else 2^a 3^b 5^c runs the generic path (BTTB_GENERIC=1 forces it, tests)
+  const char* genv = getenv("BTTB_GENERIC");
+  p->generic = (genv && atoi(genv) != 0) || !length_family(p->Lx) || !length_family(p->Ly);
+  if (p->Lx < p->mx || p->Ly < p->my || !generic_length_ok(p->Lx) || !generic_length_ok(p->Ly) ||
+      (double)p->Lx * (double)p->Ly >= 2147483648.0) {
+    rc = fail(BTTB_EINVAL,
+              "FFT lengths (%lld, %lld) unsupported for embedding (%lld, %lld): each must be >= the embedding, "
+              "of the form 2^a 3^b 5^c and at most 65536, with Lx*Ly < 2^31",
+              (long long)p->Lx, (long long)p->Ly, (long long)p->mx, (long long)p->my);
   }
   if (!rc) {
     p->Hx = p->Lx / 2 + 1;
     p->elem = dtype == BTTB_F64 ? sizeof(double2) : sizeof(float2);
-    rc = p->fx.init(p->Lx);
+    rc = p->generic ? generic_init(p) : p->fx.init(p->Lx);
   }
-  if (!rc) rc = p->fy.init(p->Ly);
+  if (!rc && !p->generic) rc = p->fy.init(p->Ly);
   if (!rc) {
     const size_t bytes = (size_t)p->nzl * p->Hx * p->Ly * p->elem;
     e = guard_alloc(&p->spectra, bytes) ? cudaErrorMemoryAllocation : cudaSuccess;
@@ -1237,13 +926,8 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
   }
   if (!rc) {
     bool ok = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) == cudaSuccess &&
               cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&p->ev_aux, cudaEventDisableTiming) == cudaSuccess;
-    for (int i = 0; i < 2 && ok; ++i)
-      ok = cudaEventCreateWithFlags(&p->ev_row[i], cudaEventDisableTiming) == cudaSuccess &&
-           cudaEventCreateWithFlags(&p->ev_col[i], cudaEventDisableTiming) == cudaSuccess;
+              cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < bttb_plan_s::kRing && ok; ++i)
       ok = cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&p->ev_in_free[i], cudaEventDisableTiming) == cudaSuccess &&
@@ -1262,13 +946,6 @@ static int plan_create_impl(bttb_plan** out, const bttb_grid* grid, const bttb_k
     } else {
       rc = build_spectra(p, host_windows);
     }
-  }
-  if (!rc && use_fused(p)) {  // the fused kernels read each warp's ky half contiguously
-    cudaError_t ce = p->dtype == BTTB_F64 ? launch_ky_split<double>(p->spectra, p->nzl * p->Hx, +1, 0)
-                                          : launch_ky_split<float>(p->spectra, p->nzl * p->Hx, +1, 0);
-    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
-    if (ce != cudaSuccess) rc = fail(BTTB_ECUDA, "spectrum layout: %s", cudaGetErrorString(ce));
-    p->fused = !rc;
   }
   if (rc) {
     std::string msg = g_err;
@@ -1377,7 +1054,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   } else if (where != BTTB_DEVICE_PTR) {
     return fail(BTTB_EINVAL, "where must be BTTB_DEVICE_PTR, BTTB_HOST_PTR, BTTB_HOST_ASYNC or BTTB_HOST_ASYNC_UNORDERED");
   }
-  // the work runs on the plan's stream (which carries the L2 window), ordered
+  // the work runs on the plan's stream, ordered
   // after everything already queued on the caller's stream and before
   // anything the caller queues next
   CU(cudaEventRecord(p->ev_in, st));
@@ -1390,7 +1067,6 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   if (where == BTTB_HOST_PTR) {
     CU(cudaMemcpyAsync(y, yd, out_elems * esz, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    if (p->pipe_err_host && *p->pipe_err_host) return fail(BTTB_ECUDA, "fused pipeline deadlock guard tripped");
   }
   return BTTB_OK;
 }
@@ -1503,17 +1179,6 @@ int bttb_layer_spectrum(bttb_plan* p, int64_t local_layer, void* host_out) {
   DeviceGuard dg(p->device);
   const size_t bytes = (size_t)p->Hx * p->Ly * p->elem;
   CU(cudaMemcpy(host_out, static_cast<char*>(p->spectra) + bytes * local_layer, bytes, cudaMemcpyDeviceToHost));
-  if (p->fused) {  // ky-split rows (fused.h) back to natural ky order
-    std::vector<char> row(p->Ly * p->elem);
-    char* h = static_cast<char*>(host_out);
-    const size_t half = (size_t)(p->Ly / 2) * p->elem;
-    for (int64_t kx = 0; kx < p->Hx; ++kx) {
-      char* r = h + (size_t)kx * p->Ly * p->elem;
-      memcpy(row.data(), r, row.size());
-      for (int64_t ky = 0; ky < p->Ly; ++ky)
-        memcpy(r + ky * p->elem, row.data() + (ky & 1) * half + (size_t)(ky >> 1) * p->elem, p->elem);
-    }
-  }
   return BTTB_OK;
 }
 

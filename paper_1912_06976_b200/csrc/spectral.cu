@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_row_c2r(RowC2RArgs a, FFTDesc<ty
   for (int it = tid; it < nitems; it += blockDim.x) {
     const int kx = it / P, cc = it - kx * P;
     const int j = j0 + 2 * cc;
-    const V* p = a.rowmajor ? in + (long long)j * a.ld_in + kx : in + (long long)kx * a.ld_in + j;
+    const V* p = in + (long long)kx * a.ld_in + j;
     V A = j < a.nrows ? p[0] : mkc<V>(T(0), T(0));
-    V B = j + 1 < a.nrows ? p[a.rowmajor ? a.ld_in : 1] : mkc<V>(T(0), T(0));
+    V B = j + 1 < a.nrows ? p[1] : mkc<V>(T(0), T(0));
     if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
       A.y = T(0);
       B.y = T(0);
@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
     if constexpr (ACCS) dhs[t + nt * k] = v[k]; else dh[k] = v[k];
   }
   const V* Sb = static_cast<const V*>(a.S) + (long long)kxc * a.lds;
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kxc * (a.rowmajor ? 1 : a.ldw);
-  const long long qstride = a.rowmajor ? a.ldw : 1;
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kxc * a.ldw;
+  const long long qstride = 1;
   for (int r = 0; r < a.K; ++r) {
     const V* sc = Sb + (long long)r * a.s_rstride;
 #pragma unroll
@@ -337,10 +337,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], ybytes);
       tma_load(ybuf, Yb + (long long)(r + 1) * a.y_rstride, ybytes, &bars[0], pol);
-      if (a.ahead > 1 && r + a.ahead < K) {
-        l2_prefetch(Yb + (long long)(r + a.ahead) * a.y_rstride, ybytes);
-        l2_prefetch(Sb + (long long)(r + a.ahead) * a.s_rstride, sbytes);
-      }
     }
     PL::fft(v, sm, t, d);
     mbar_wait(&bars[1], r & 1);
@@ -377,162 +373,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   }
 }
 
-// Forward column stage without the Y staging buffer (opt-in BTTB_FWD_NOY=1):
-// the layer's Y column is read straight into registers at the start of each
-// layer, so shared memory holds only the exchange buffer and one spectrum
-// column (67 KB at fp64 L=2048) and three CTAs fit an SM (MINB = 3, 168
-// registers) -- the other two CTAs cover the load latency instead of a TMA
-// prefetch.  Shared: [exchange Ls][S L][mbarrier].
-template <class PL, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_noy(ColFwdArgs a, FFTDesc<typename PL::Scalar> d) {
-  using T = typename PL::Scalar;
-  using V = cplx<T>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = (PL::slots(L) + 1) & ~1;
-  V* sm = reinterpret_cast<V*>(smraw);
-  V* sbuf = sm + Ls;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + L);
-  const int t = threadIdx.x;
-  const int kx = blockIdx.x, b = blockIdx.y;
-  const int K = a.K, nv = a.nvalid;
-  const uint32_t sbytes = L * sizeof(V);
-  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
-  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
-  const uint64_t pol = policy_evict_first();
-  if (t == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    mbar_arrive_expect_tx(bar, sbytes);
-    tma_load(sbuf, Sb, sbytes, bar, pol);
-  }
-  __syncthreads();
-  V acc[E], v[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
-  for (int r = 0; r < K; ++r) {
-    const V* yr = Yb + (long long)r * a.y_rstride;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int q = t + NT * k;
-      v[k] = q < nv ? __ldcs(yr + q) : mkc<V>(T(0), T(0));
-    }
-    PL::fft(v, sm, t, d);
-    mbar_wait(bar, r & 1);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const V w = sbuf[t + NT * k];
-      acc[k].x += w.x * v[k].x - w.y * v[k].y;
-      acc[k].y += w.x * v[k].y + w.y * v[k].x;
-    }
-    __syncthreads();
-    if (t == 0 && r + 1 < K) {
-      fence_proxy_async();
-      mbar_arrive_expect_tx(bar, sbytes);
-      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, bar, pol);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
-  PL::fft(acc, sm, t, d);
-  V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    const int j = t + NT * k;
-    if (j < a.nout) {
-      V val = conjv(acc[k]);
-      if (a.accumulate) val = val + wc[j];
-      wc[j] = val;
-    }
-  }
-}
-
-// Double-buffered forward column stage (plans whose column input fits the
-// first half of the transform, nvalid <= L/2, as for every zero-padded
-// embedding at L >= 2n-1): the next layer's Y column is loaded straight into
-// registers (E/2 elements per thread) while the team transforms the current
-// one, and the spectrum columns rotate through TWO shared buffers, so each
-// bulk copy is issued a whole layer ahead of its use instead of during the
-// current layer's FFT.  Shared: [exchange Ls][S0 L][S1 L][2 mbarriers].
-template <class PL, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_db(ColFwdArgs a, FFTDesc<typename PL::Scalar> d) {
-  using T = typename PL::Scalar;
-  using V = cplx<T>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L, EH = E / 2;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = (PL::slots(L) + 1) & ~1;
-  V* sm = reinterpret_cast<V*>(smraw);
-  V* sbuf = sm + Ls;  // two spectrum buffers of L
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + 2 * L);
-  const int t = threadIdx.x;
-  const int kx = blockIdx.x, b = blockIdx.y;
-  const int K = a.K, nv = a.nvalid;
-  const uint32_t sbytes = L * sizeof(V);
-  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
-  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
-  const uint64_t pol = policy_evict_first();
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    for (int i = 0; i < 2 && i < K; ++i) {
-      mbar_arrive_expect_tx(&bars[i], sbytes);
-      tma_load(sbuf + i * L, Sb + (long long)i * a.s_rstride, sbytes, &bars[i], pol);
-    }
-  }
-  V yn[EH];
-#pragma unroll
-  for (int k = 0; k < EH; ++k) {
-    const int q = t + NT * k;
-    yn[k] = q < nv ? __ldcs(Yb + q) : mkc<V>(T(0), T(0));
-  }
-  __syncthreads();
-  V acc[E], v[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
-  for (int r = 0; r < K; ++r) {
-#pragma unroll
-    for (int k = 0; k < E; ++k) v[k] = k < EH ? yn[k] : mkc<V>(T(0), T(0));
-    if (r + 1 < K) {
-      const V* yr = Yb + (long long)(r + 1) * a.y_rstride;
-#pragma unroll
-      for (int k = 0; k < EH; ++k) {
-        const int q = t + NT * k;
-        yn[k] = q < nv ? __ldcs(yr + q) : mkc<V>(T(0), T(0));
-      }
-    }
-    PL::fft(v, sm, t, d);
-    const int bi = r & 1;
-    mbar_wait(&bars[bi], (r >> 1) & 1);
-    const V* sb = sbuf + bi * L;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const V w = sb[t + NT * k];
-      acc[k].x += w.x * v[k].x - w.y * v[k].y;
-      acc[k].y += w.x * v[k].y + w.y * v[k].x;
-    }
-    __syncthreads();
-    if (t == 0 && r + 2 < K) {
-      fence_proxy_async();
-      mbar_arrive_expect_tx(&bars[bi], sbytes);
-      tma_load(sbuf + bi * L, Sb + (long long)(r + 2) * a.s_rstride, sbytes, &bars[bi], pol);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
-  PL::fft(acc, sm, t, d);
-  V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    const int j = t + NT * k;
-    if (j < a.nout) {
-      V val = conjv(acc[k]);
-      if (a.accumulate) val = val + wc[j];
-      wc[j] = val;
-    }
-  }
-}
-
 template <class PL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDesc<typename PL::Scalar> d) {
   using T = typename PL::Scalar;
@@ -564,9 +404,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
   }
   __syncthreads();
   PL::fft(dh, sm, t, d);
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw) +
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw +
           (long long)r0 * a.w_rstride;
-  const long long qstride = a.rowmajor ? a.ldw : 1;
+  const long long qstride = 1;
   for (int r = 0; r < K; ++r) {
     mbar_wait(&bars[0], r & 1);
 #pragma unroll
@@ -580,7 +420,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[0], sbytes);
       tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[0], pol);
-      if (a.ahead > 1 && r + a.ahead < K) l2_prefetch(Sb + (long long)(r + a.ahead) * a.s_rstride, sbytes);
     }
     PL::fft(v, sm, t, d);
     V* wc = Wb + (long long)r * a.w_rstride;
@@ -618,104 +457,6 @@ __device__ __forceinline__ void split4(double2 a, uint32_t* r) {
 }
 __device__ __forceinline__ double2 join4(const uint32_t* r) {
   return make_double2(__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2]));
-}
-
-template <class PL, int MINB>
-__global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_fwd_tmem(ColFwdArgs a, FFTDesc<double> d) {
-  using V = double2;
-  using TC = TmemCfg<PL>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = (PL::slots(L) + 1) & ~1;
-  V* sm = reinterpret_cast<V*>(smraw);
-  V* sbuf = sm + Ls;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + L);
-  uint32_t* taddr_s = reinterpret_cast<uint32_t*>(bar + 1);
-  const int t = threadIdx.x, warp = t / 32;
-  const bool active = t < NT;
-  const int kx = blockIdx.x, b = blockIdx.y;
-  const uint32_t sbytes = L * sizeof(V);
-  const V* Yb = static_cast<const V*>(a.Y) + (long long)b * a.y_bstride + (long long)kx * a.ldy;
-  const V* Sb = static_cast<const V*>(a.S) + (long long)kx * a.lds;
-  const uint64_t pol = policy_evict_first();
-  if (warp == 0) tmem_alloc<TC::NCOLS>(taddr_s);
-  if (t == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    mbar_arrive_expect_tx(bar, sbytes);
-    tma_load(sbuf, Sb, sbytes, bar, pol);
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t ta = *taddr_s + ((uint32_t)(32 * (warp & 3)) << 16);
-  {
-    uint32_t z[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) z[i] = 0u;
-#pragma unroll
-    for (int g = 0; g < TC::GROUPS; ++g) tmem_st16(ta + 16 * g, z);
-    tmem_wait_st();
-  }
-  V v[E];
-  for (int r = 0; r < a.K; ++r) {
-    const V* yc = Yb + (long long)r * a.y_rstride;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int q = t + NT * k;
-      v[k] = active && q < a.nvalid ? yc[q] : mkc<V>(0.0, 0.0);
-    }
-    PL::fft_masked(v, sm, t, d, active);
-    mbar_wait(bar, r & 1);
-#pragma unroll
-    for (int g = 0; g < TC::GROUPS; ++g) {
-      uint32_t acc[16];
-      tmem_ld16(ta + 16 * g, acc);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int k = 4 * g + c;
-        V o = join4(acc + 4 * c);
-        const V w = active ? sbuf[t + NT * k] : mkc<V>(0.0, 0.0);
-        o.x += w.x * v[k].x - w.y * v[k].y;
-        o.y += w.x * v[k].y + w.y * v[k].x;
-        split4(o, acc + 4 * c);
-      }
-      tmem_st16(ta + 16 * g, acc);
-    }
-    tmem_wait_st();
-    __syncthreads();
-    if (t == 0 && r + 1 < a.K) {
-      fence_proxy_async();
-      mbar_arrive_expect_tx(bar, sbytes);
-      tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, bar, pol);
-    }
-  }
-#pragma unroll
-  for (int g = 0; g < TC::GROUPS; ++g) {
-    uint32_t acc[16];
-    tmem_ld16(ta + 16 * g, acc);
-    tmem_wait_ld();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[4 * g + c] = conjv(join4(acc + 4 * c));
-  }
-  PL::fft_masked(v, sm, t, d, active);
-  if (active) {
-    V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int j = t + NT * k;
-      if (j < a.nout) {
-        V val = conjv(v[k]);
-        if (a.accumulate) val = val + wc[j];
-        wc[j] = val;
-      }
-    }
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  if (warp == 0) tmem_dealloc<TC::NCOLS>(*taddr_s);
 }
 
 template <class PL, int MINB>
@@ -763,9 +504,9 @@ __global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_tra_tmem(ColTraA
     tmem_st16(ta + 16 * g, u);
   }
   tmem_wait_st();
-  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * (a.rowmajor ? 1 : a.ldw) +
+  V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw +
           (long long)r0 * a.w_rstride;
-  const long long qstride = a.rowmajor ? a.ldw : 1;
+  const long long qstride = 1;
   for (int r = 0; r < K; ++r) {
     mbar_wait(bar, r & 1);
 #pragma unroll
@@ -802,162 +543,6 @@ __global__ void __launch_bounds__(TmemCfg<PL>::NTR, MINB) k_col_tra_tmem(ColTraA
   __syncthreads();
   tmem_fence_after();
   if (warp == 0) tmem_dealloc<TC::NCOLS>(*taddr_s);
-}
-
-// ---------------------------------------------------------------------------
-// Persistent, TMA double-buffered row passes (compile-time plans, one row pair
-// per iteration, one team per CTA).  Thread 0 bulk-copies the rows of the pair
-// two iterations ahead into the stage just consumed, so the contiguous row
-// loads overlap the FFTs.  Shared layout:
-//   [exchange Ls V][stage 0: row a, row b][stage 1: row a, row b][2 mbarriers]
-// ---------------------------------------------------------------------------
-template <class PL, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k_row_r2c_tma(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, int rowcap) {
-  using T = typename PL::Scalar;
-  using V = cplx<T>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = (PL::slots(L) + 1) & ~1;  // keep the TMA staging buffers 16-byte aligned
-  V* sm = reinterpret_cast<V*>(smraw);
-  T* stage0 = reinterpret_cast<T*>(sm + Ls);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + 4 * rowcap);
-  const int t = threadIdx.x;
-  const int npairs = (a.nrows + 1) / 2, total = npairs * a.nslabs;
-  const uint64_t pol = policy_evict_first();
-  auto row_ptr = [&](int item, int which) {
-    const int s = item / npairs, q = 2 * (item - s * npairs) + which;
-    return static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride + (long long)(s % a.spb) * a.in_sstride +
-           (long long)q * a.ld_in;
-  };
-  auto has_b = [&](int item) { return 2 * (item % npairs) + 1 < a.nrows; };
-  auto issue = [&](int item, int st) {
-    const uint32_t bytes = a.nvalid * sizeof(T);
-    T* dst = stage0 + st * 2 * rowcap;
-    const bool b2 = has_b(item);
-    mbar_arrive_expect_tx(&bars[st], b2 ? 2 * bytes : bytes);
-    tma_load(dst, row_ptr(item, 0), bytes, &bars[st], pol);
-    if (b2) tma_load(dst + rowcap, row_ptr(item, 1), bytes, &bars[st], pol);
-  };
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
-    if ((int)(blockIdx.x + gridDim.x) < total) issue(blockIdx.x + gridDim.x, 1);
-  }
-  __syncthreads();
-  V v[E];
-  int it = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
-    const int st = it & 1;
-    mbar_wait(&bars[st], (it >> 1) & 1);
-    const T* ra = stage0 + st * 2 * rowcap;
-    const T* rb = ra + rowcap;
-    const bool vb = has_b(item);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int i = t + NT * k;
-      const bool inb = i < a.nvalid;
-      v[k] = mkc<V>(inb ? ra[i] : T(0), inb && vb ? rb[i] : T(0));
-    }
-    __syncthreads();
-    if (t == 0 && item + 2 * (int)gridDim.x < total) {
-      fence_proxy_async();
-      issue(item + 2 * gridDim.x, st);
-    }
-    PL::fft(v, sm, t, d);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
-    __syncthreads();
-    const int s = item / npairs, q = 2 * (item - s * npairs);
-    V* out = static_cast<V*>(a.out) + (long long)s * a.out_sstride + q;
-    for (int kx = t; kx < a.Hx; kx += NT) {
-      const V zk = sm[PL::slot(kx)];
-      const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
-      const T h = T(0.5);
-      V* o = out + (long long)kx * a.ld_out;
-      o[0] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
-      if (vb) o[1] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
-    }
-  }
-}
-
-template <class PL, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k_row_c2r_tma(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, int rowcap) {
-  using T = typename PL::Scalar;
-  using V = cplx<T>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int Ls = (PL::slots(L) + 1) & ~1;  // keep the TMA staging buffers 16-byte aligned
-  V* sm = reinterpret_cast<V*>(smraw);
-  V* stage0 = sm + Ls;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + 4 * rowcap);
-  const int t = threadIdx.x;
-  const int npairs = (a.nrows + 1) / 2, total = npairs * a.nslabs;
-  const uint64_t pol = policy_evict_first();
-  const uint32_t bytes = rowcap * sizeof(V);
-  auto row_ptr = [&](int item, int which) {
-    const int s = item / npairs, j = 2 * (item - s * npairs) + which;
-    return static_cast<const V*>(a.in) + (long long)s * a.in_sstride + (long long)j * a.ld_in;
-  };
-  auto has_b = [&](int item) { return 2 * (item % npairs) + 1 < a.nrows; };
-  auto issue = [&](int item, int st) {
-    V* dst = stage0 + st * 2 * rowcap;
-    const bool b2 = has_b(item);
-    mbar_arrive_expect_tx(&bars[st], b2 ? 2 * bytes : bytes);
-    tma_load(dst, row_ptr(item, 0), bytes, &bars[st], pol);
-    if (b2) tma_load(dst + rowcap, row_ptr(item, 1), bytes, &bars[st], pol);
-  };
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
-    if ((int)(blockIdx.x + gridDim.x) < total) issue(blockIdx.x + gridDim.x, 1);
-  }
-  __syncthreads();
-  V v[E];
-  int it = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
-    const int st = it & 1;
-    mbar_wait(&bars[st], (it >> 1) & 1);
-    const V* ra = stage0 + st * 2 * rowcap;
-    const V* rb = ra + rowcap;
-    const bool vb = has_b(item);
-    // build Z = A + iB over the full length from the two half spectra
-    for (int kx = t; kx < a.Hx; kx += NT) {
-      V A = ra[kx];
-      V B = vb ? rb[kx] : mkc<V>(T(0), T(0));
-      if (kx == 0 || 2 * kx == L) {  // Hermitian projection (.real semantics)
-        A.y = T(0);
-        B.y = T(0);
-      }
-      sm[PL::slot(kx)] = mkc<V>(A.x - B.y, A.y + B.x);
-      if (kx >= 1 && kx <= L - a.Hx) sm[PL::slot(L - kx)] = mkc<V>(A.x + B.y, B.x - A.y);
-    }
-    __syncthreads();
-    if (t == 0 && item + 2 * (int)gridDim.x < total) {
-      fence_proxy_async();
-      issue(item + 2 * gridDim.x, st);
-    }
-#pragma unroll
-    for (int k = 0; k < E; ++k) v[k] = conjv(sm[PL::slot(t + NT * k)]);
-    PL::fft(v, sm, t, d);
-    const int s = item / npairs, j = 2 * (item - s * npairs);
-    T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
-    T* oa = out + (long long)j * a.ld_out;
-    T* ob = oa + a.ld_out;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int i = t + NT * k;
-      if (i < a.nout) {
-        __stcs(oa + i, v[k].x);
-        if (vb) __stcs(ob + i, -v[k].y);
-      }
-    }
-    __syncthreads();  // the next fill overwrites sm
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1134,100 +719,6 @@ __global__ void __launch_bounds__(MAXT, MINB)
       tma_store_wait_read();
     }
   }
-}
-
-// Persistent R2C: each CTA walks row pairs with a stride of gridDim.x; thread 0
-// bulk-copies the NEXT pair's two rows into a row stage while the team
-// transforms the current pair, then the tile leaves by tensor-TMA store.
-// Shared: [exchange/stage tile (RowTile::slots)][row stage 2 x rowcap reals][mbarrier].
-template <class PL, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB)
-    k_row_r2c_pt(RowR2CArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap omap, int rowcap) {
-  using T = typename PL::Scalar;
-  using V = cplx<T>;
-  using RT = RowTile<PL>;
-  constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NI = RT::NI;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  V* sm = reinterpret_cast<V*>(smraw);
-  T* rows = reinterpret_cast<T*>(sm + RT::slots((PL::slots(L) + 1) & ~1));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(rows + 2 * rowcap);
-  const int t = threadIdx.x;
-  const int npairs = (a.nrows + 1) / 2, total = npairs * a.nslabs;
-  const uint64_t pol = policy_evict_first();
-  const uint32_t bytes = a.nvalid * sizeof(T);
-  auto row_ptr = [&](int item, int which) {
-    const int s = item / npairs, q = 2 * (item - s * npairs) + which;
-    return static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride + (long long)(s % a.spb) * a.in_sstride +
-           (long long)q * a.ld_in;
-  };
-  auto has_b = [&](int item) { return 2 * (item % npairs) + 1 < a.nrows; };
-  auto issue = [&](int item) {
-    const bool b2 = has_b(item);
-    mbar_arrive_expect_tx(bar, b2 ? 2 * bytes : bytes);
-    tma_load(rows, row_ptr(item, 0), bytes, bar, pol);
-    if (b2) tma_load(rows + rowcap, row_ptr(item, 1), bytes, bar, pol);
-  };
-  if (t == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    if ((int)blockIdx.x < total) issue(blockIdx.x);
-  }
-  __syncthreads();
-  const T h = T(0.5);
-  int it = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
-    mbar_wait(bar, it & 1);
-    const bool vb = has_b(item);
-    V v[E];
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int i = t + NT * k;
-      const bool inb = i < a.nvalid;
-      v[k] = mkc<V>(inb ? rows[i] : T(0), inb && vb ? rows[rowcap + i] : T(0));
-    }
-    __syncthreads();  // rows consumed
-    if (t == 0 && item + (int)gridDim.x < total) {
-      fence_proxy_async();
-      issue(item + gridDim.x);
-    }
-    // the previous tile's TMA store may still be reading sm: wait only right
-    // before the first exchange overwrites it (after the first radix pass)
-    PL::fft_hook(v, sm, t, d, [&] {
-      if (t == 0 && it > 0) tma_store_wait_read();
-    });
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < E; ++k) sm[PL::slot(t + NT * k)] = v[k];
-    __syncthreads();
-    V A[NI], B[NI];
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const int kx = t + NT * i;
-      if (kx < HX) {
-        const V zk = sm[PL::slot(kx)];
-        const V zm = sm[PL::slot(kx == 0 ? 0 : L - kx)];
-        A[i] = mkc<V>(h * (zk.x + zm.x), h * (zk.y - zm.y));
-        B[i] = mkc<V>(h * (zk.y + zm.y), h * (zm.x - zk.x));
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const int kx = t + NT * i;
-      if (kx < HX) {
-        sm[2 * kx] = A[i];
-        sm[2 * kx + 1] = B[i];
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (t == 0) {
-      const int s = item / npairs, qa = 2 * (item - s * npairs);
-      for (int kx0 = 0; kx0 < HX; kx0 += RT::BOXK) tma_store_3d(&omap, sm + 2 * kx0, 2 * qa, kx0, s);
-      tma_store_commit();
-    }
-  }
-  if (t == 0) tma_store_wait_read();
 }
 
 // The FFT input is read straight from the staged tile: element n of the
@@ -1470,25 +961,11 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_spec(ColSpecArgs a, FFTDesc<
 // ---------------------------------------------------------------------------
 template <class P> struct Tag { using type = P; };
 
-// opt-in (BTTB_COL_E10=1): measured slower on C4 fp64 (9.2 vs 7.7 ms/step) --
-// the third shared-memory exchange costs more than the occupancy it buys
-bool row_e10() {
-  static const bool on = getenv("BTTB_ROW_E10") && atoi(getenv("BTTB_ROW_E10")) != 0;
-  return on;
-}
-
-bool col_e10() {
-  static const bool on = getenv("BTTB_COL_E10") && atoi(getenv("BTTB_COL_E10")) != 0;
-  return on;
-}
-
 // COL selects the plan of the accumulating column kernels where it differs
 // (fp64 L=2000: 10 elements per thread keeps the E-element accumulator cheap)
 template <class T, bool COL = false, bool ROW = false, class F>
 cudaError_t with_plan(int L, int E, F&& f) {
   if constexpr (sizeof(T) == 8) {
-    if (COL && L == 2000 && col_e10()) return f(Tag<SPlanG<double, 10, 40, 10, 10, 10, 2>>{});
-    if (ROW && L == 2000 && row_e10()) return f(Tag<SPlanG<double, 10, 40, 10, 10, 10, 2>>{});
     switch (L) {
       case 2048: return f(Tag<SPlan<double, 16, 16, 16, 16, 8>>{});
       case 2000: return f(Tag<SPlan<double, 20, 20, 20, 20, 5>>{});
@@ -1543,7 +1020,6 @@ int static_radices(int L, bool fp64, int* out) {
 }
 
 }  // namespace bttb
-#include "pipeline.cuh"
 namespace bttb {
 
 // Fixed launch shapes of the compile-time plans: teams per CTA and the
@@ -1594,20 +1070,9 @@ template <class PL> struct Shape {
 bool env_flag(const char* name, bool dflt);
 
 // fp32 row passes move four rows per CTA (32-byte box rows); BTTB_QUAD=0 off
-// (fp64: opt-in BTTB_QUAD64=1, its box rows are already full sectors)
-template <class T> bool quad_rows() {
-  if constexpr (sizeof(T) == 4) {
-    static const bool on = !(getenv("BTTB_QUAD") && atoi(getenv("BTTB_QUAD")) == 0);
-    return on;
-  } else {
-    static const bool on = env_flag("BTTB_QUAD64", false);
-    return on;
-  }
-}
-
-// double-buffered forward column stage (k_col_fwd_db): BTTB_FWD_DB=1 opt-in
-bool fwd_db_ok() {
-  static const bool on = getenv("BTTB_FWD_DB") && atoi(getenv("BTTB_FWD_DB")) != 0;
+// (fp64 box rows are already full sectors: four-row fp64 boxes measured no gain)
+bool quad_rows() {
+  static const bool on = !(getenv("BTTB_QUAD") && atoi(getenv("BTTB_QUAD")) == 0);
   return on;
 }
 
@@ -1621,13 +1086,6 @@ bool c2r_mirror_ok() {
 
 bool tma_ok() {
   static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
-  return ok;
-}
-
-// persistent TMA row passes: opt-in (BTTB_ROW_TMA=1); measured slower than the
-// one-CTA-per-pair kernels on C4 (8.73 vs 8.50 ms/step fp64)
-bool row_tma_ok() {
-  static const bool ok = tma_ok() && getenv("BTTB_ROW_TMA") && atoi(getenv("BTTB_ROW_TMA")) != 0;
   return ok;
 }
 
@@ -1706,24 +1164,16 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// TMEM-resident column state.  Transpose (data spectrum in TMEM): default on,
-// measured 2.84 vs 2.95 ms per C4 fp64 transpose; forward (accumulator in
-// TMEM): opt-in, measured 2.98 vs 2.60 ms.  BTTB_TMEM=0/1 overrides both.
+// TMEM-resident column state of the transpose (data spectrum in TMEM) for
+// teams that are not whole warps (L = 2000): default on, measured 2.84 vs
+// 2.95 ms per C4 fp64 transpose (BTTB_TMEM_TRA=0 off).  The forward variant
+// (accumulator in TMEM) measured 2.98 vs 2.60 ms and was removed.
 bool env_flag(const char* name, bool dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) != 0 : dflt;
 }
-bool tmem_fwd_ok() {
-  static const bool on = env_flag("BTTB_TMEM_FWD", env_flag("BTTB_TMEM", false));
-  return on;
-}
 bool tmem_tra_ok() {
   static const bool on = env_flag("BTTB_TMEM_TRA", env_flag("BTTB_TMEM", true));
-  return on;
-}
-
-bool persistent_r2c() {
-  static const bool on = getenv("BTTB_R2C_PERSIST") && atoi(getenv("BTTB_R2C_PERSIST")) != 0;  // measured slower (7.61 vs 7.26 ms)
   return on;
 }
 
@@ -1790,44 +1240,21 @@ cudaError_t launch_row_r2c(const RowR2CArgs& a, const FFTDesc<T>& d, int E, cuda
   return with_plan<T, false, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && PL::NT >= 32) {
-      const size_t esz = sizeof(T);
-      if (row_tma_ok() && al16(a.in) && (a.nvalid * esz) % 16 == 0 && (a.ld_in * esz) % 16 == 0 &&
-          (a.in_sstride * esz) % 16 == 0 && (a.in_bstride * esz) % 16 == 0) {
-        auto kern = k_row_r2c_tma<PL, PL::NT, Shape<PL>::rowtma_minb>;
-        const int rowcap = (a.nvalid + 1) & ~1;
-        const size_t smem = (size_t)((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 4 * (size_t)rowcap * esz + 16;
-        cudaError_t e = set_smem(kern, smem);
-        if (e != cudaSuccess) return e;
-        const int items = (a.nrows + 1) / 2 * a.nslabs;
-        kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, rowcap);
-        return cudaGetLastError();
-      }
       CUtensorMap omap;
-      if (t2d_ok() && quad_rows<T>() && a.Hx <= 65535 &&
-          encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride, 4)) {
-        auto kern = k_row_r2c_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
-        const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
-        cudaError_t e = set_smem(kern, smem);
-        if (e != cudaSuccess) return e;
-        dim3 grd((a.nrows + 3) / 4, a.nslabs);
-        kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, omap);
-        return cudaGetLastError();
+      if constexpr (sizeof(T) == 4) {
+        if (t2d_ok() && quad_rows() && a.Hx <= 65535 &&
+            encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride, 4)) {
+          auto kern = k_row_r2c_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
+          const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
+          cudaError_t e = set_smem(kern, smem);
+          if (e != cudaSuccess) return e;
+          dim3 grd((a.nrows + 3) / 4, a.nslabs);
+          kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, omap);
+          return cudaGetLastError();
+        }
       }
       if (t2d_ok() && a.Hx <= 65535 &&
           encode_rowpair_map<T>(&omap, a.out, a.nrows, a.Hx, a.nslabs, a.ld_out, a.out_sstride)) {
-        const size_t esz = sizeof(T);
-        if (persistent_r2c() && al16(a.in) && (a.nvalid * esz) % 16 == 0 && (a.ld_in * esz) % 16 == 0 &&
-            (a.in_sstride * esz) % 16 == 0 && (a.in_bstride * esz) % 16 == 0) {
-          auto kern = k_row_r2c_pt<PL, PL::NT, Shape<PL>::t2d_minb>;
-          const int rowcap = (a.nvalid + 3) & ~3;
-          const size_t smem = (size_t)RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) +
-                              2 * (size_t)rowcap * esz + 16;
-          cudaError_t e = set_smem(kern, smem);
-          if (e != cudaSuccess) return e;
-          const int items = (a.nrows + 1) / 2 * a.nslabs;
-          kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, omap, rowcap);
-          return cudaGetLastError();
-        }
         constexpr int TM = Shape<PL>::t2d_teams;
         auto kern = k_row_r2c_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM>;
         const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>);
@@ -1855,60 +1282,34 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
   return with_plan<T, false, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
     if constexpr (PL::kStatic && PL::NT >= 32) {
-      const size_t esz = sizeof(cplx<T>);
-      const int rowcap = (a.Hx + 1) & ~1;
-      if (row_tma_ok() && a.rowmajor && al16(a.in) && a.ld_in >= rowcap && (a.ld_in * esz) % 16 == 0 &&
-          (rowcap * esz) % 16 == 0 && (a.in_sstride * esz) % 16 == 0) {
-        auto kern = k_row_c2r_tma<PL, PL::NT, Shape<PL>::rowtma_minb>;
-        const size_t smem = (size_t)((PL::slots(d.L) + 1) & ~1) * esz + 4 * (size_t)rowcap * esz + 16;
-        cudaError_t e = set_smem(kern, smem);
-        if (e != cudaSuccess) return e;
-        const int items = (a.nrows + 1) / 2 * a.nslabs;
-        kern<<<persistent_grid(kern, PL::NT, smem, items), PL::NT, smem, st>>>(a, d, rowcap);
-        return cudaGetLastError();
-      }
       CUtensorMap imap;
-      if (t2d_ok() && quad_rows<T>() && !a.rowmajor &&
-          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 4)) {
-        if constexpr (PL::kR16x16x8 && PL::kPerPass) {
-          if (a.tw_816 && c2r_mirror_ok()) {
-            using PLC = SPlanT<T, 16, C2R_MIRROR_PAD(T), true, 8, 16, 16>;
-            auto kern = k_row_c2r_mirror<PL, PLC, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
-            const size_t smem =
-                (size_t)2 * RowTile<PL>::slots((PLC::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
-            cudaError_t e = set_smem(kern, smem);
-            if (e != cudaSuccess) return e;
-            dim3 grd((a.nrows + 3) / 4, a.nslabs);
-            kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
-            return cudaGetLastError();
+      if constexpr (sizeof(T) == 4) {
+        if (t2d_ok() && quad_rows() &&
+            encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 4)) {
+          if constexpr (PL::kR16x16x8 && PL::kPerPass) {
+            if (a.tw_816 && c2r_mirror_ok()) {
+              using PLC = SPlanT<T, 16, C2R_MIRROR_PAD(T), true, 8, 16, 16>;
+              auto kern = k_row_c2r_mirror<PL, PLC, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
+              const size_t smem =
+                  (size_t)2 * RowTile<PL>::slots((PLC::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
+              cudaError_t e = set_smem(kern, smem);
+              if (e != cudaSuccess) return e;
+              dim3 grd((a.nrows + 3) / 4, a.nslabs);
+              kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
+              return cudaGetLastError();
+            }
           }
+          auto kern = k_row_c2r_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
+          const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
+          cudaError_t e = set_smem(kern, smem);
+          if (e != cudaSuccess) return e;
+          dim3 grd((a.nrows + 3) / 4, a.nslabs);
+          kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
+          return cudaGetLastError();
         }
-        auto kern = k_row_c2r_t2d<PL, 2 * PL::NT, Shape<PL>::quad_minb, 2, true>;
-        const size_t smem = (size_t)2 * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 32;
-        cudaError_t e = set_smem(kern, smem);
-        if (e != cudaSuccess) return e;
-        dim3 grd((a.nrows + 3) / 4, a.nslabs);
-        kern<<<grd, 2 * PL::NT, smem, st>>>(a, d, imap);
-        return cudaGetLastError();
-      }
-      // BTTB_C2R_SPLIT=1 (fp64 only: fp32 rows would be 8-byte box rows, below
-      // the tensor-TMA minimum): the two rows as separate [kx] boxes, so the
-      // tile reads are conflict-free -- measured slower (C4 fp64 C2R 0.71 vs
-      // 0.69 ms: the half-sector box rows double the L2 requests)
-      static const bool split_env = env_flag("BTTB_C2R_SPLIT", false);
-      if (sizeof(T) == 8 && split_env && t2d_ok() && !a.rowmajor &&
-          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 1)) {
-        constexpr int TM = Shape<PL>::t2d_teams;
-        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM, false, sizeof(T) == 8>;
-        const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
-        cudaError_t e = set_smem(kern, smem);
-        if (e != cudaSuccess) return e;
-        dim3 grd(((a.nrows + 1) / 2 + TM - 1) / TM, a.nslabs);
-        kern<<<grd, TM * PL::NT, smem, st>>>(a, d, imap);
-        return cudaGetLastError();
       }
       constexpr bool SPLIT = false;
-      if (t2d_ok() && !a.rowmajor &&
+      if (t2d_ok() &&
           encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, SPLIT ? 1 : 2)) {
         constexpr int TM = Shape<PL>::t2d_teams;
         if constexpr (PL::kR16x16x8 && PL::kPerPass) {
@@ -1949,41 +1350,10 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
   if (a.nbatch <= 0 || a.K <= 0) return cudaSuccess;
   return with_plan<T, true>(d.L, E, [&](auto tag) {
     using PL = typename decltype(tag)::type;
-    // (whole-warp teams, e.g. 2048 with 128 threads, measured no gain: 4.18 vs 4.14 ms/step)
-    if constexpr (PL::kStatic && PL::NT >= 32 && PL::NT < 128 && PL::NT % 32 != 0 && sizeof(T) == 8 &&
-                  (PL::E * 4) % 16 == 0) {
-      if (tma_ok() && tmem_fwd_ok()) {
-        auto kern = k_col_fwd_tmem<PL, 3>;
-        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * 16 + 16;
-        cudaError_t e = set_smem(kern, smem);
-        if (e != cudaSuccess) return e;
-        dim3 grd(a.Hx, a.nbatch), blk(TmemCfg<PL>::NTR);
-        kern<<<grd, blk, smem, st>>>(a, d);
-        return cudaGetLastError();
-      }
-    }
     if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
           (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
-        if (env_flag("BTTB_FWD_NOY", false)) {
-          auto kern = k_col_fwd_noy<PL, Shape<PL>::col_threads, Shape<PL>::tra_minb>;
-          const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * esz + 16;
-          cudaError_t e = set_smem(kern, smem);
-          if (e != cudaSuccess) return e;
-          dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
-          kern<<<grd, blk, smem, st>>>(a, d);
-          return cudaGetLastError();
-        }
-        if (fwd_db_ok() && 2 * a.nvalid <= d.L && PL::E % 2 == 0) {
-          auto kern = k_col_fwd_db<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
-          const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + 2 * d.L) * esz + 16;
-          cudaError_t e = set_smem(kern, smem);
-          if (e != cudaSuccess) return e;
-          dim3 grd(a.Hx, a.nbatch), blk(PL::NT);
-          kern<<<grd, blk, smem, st>>>(a, d);
-          return cudaGetLastError();
-        }
         auto kern = k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
@@ -2071,83 +1441,6 @@ cudaError_t launch_col_spec(const ColSpecArgs& a, const FFTDesc<double>& d, int 
   });
 }
 
-// ---------------------------------------------------------------------------
-// Fused layer pipeline launchers (pipeline.cuh)
-// ---------------------------------------------------------------------------
-#ifndef PIPE_TEAMS
-#define PIPE_TEAMS 3  // teams (128 threads each) per persistent CTA
-#endif
-
-int pipe_grid() { return sm_count(); }
-int pipe_teams() { return PIPE_TEAMS; }
-int pipe_counter_ints(int nz) { return pipe_err_index(nz, sm_count()) + 1; }
-
-// opt-in (BTTB_PIPE=1): correct (tests/test_gpu_pipeline.py) but measured
-// slower than the staged kernels on C4 fp64 at 2048^2 -- 5.74 vs 4.14 ms/step
-// with a 3-slot ring: its column/row items cost ~2.0 vs ~1.55 us of SM time,
-// as three teams per SM without shared memory for TMA double buffering leave
-// the L2 latency of every item exposed.
-bool pipe_enabled() {
-  static const bool on = env_flag("BTTB_PIPE", false);
-  return on;
-}
-
-template <class PL> constexpr bool pipe_plan() {
-  if constexpr (PL::kStatic) {
-    return PL::NT >= 64 && PL::NT <= pipe::TT && (PL::E * pipe::Words<cplx<typename PL::Scalar>>::W) % 16 == 0;
-  } else {
-    return false;
-  }
-}
-
-template <class T>
-bool pipe_supported(int L, int Hx) {
-  if (!pipe_enabled()) return false;
-  bool ok = false;
-  with_plan<T>(L, 0, [&](auto tag) {
-    using PL = typename decltype(tag)::type;
-    if constexpr (pipe_plan<PL>()) {
-      const int G = sm_count();
-      const int per_cta = (Hx + G - 1) / G;
-      ok = per_cta * pipe::Cfg<PL>::COLS <= 512;
-    }
-    return cudaSuccess;
-  });
-  return ok;
-}
-
-template <class T>
-cudaError_t launch_pipe(int mode, const PipeArgs& a, const FFTDesc<T>& d, cudaStream_t st) {
-  return with_plan<T>(d.L, 0, [&](auto tag) -> cudaError_t {
-    using PL = typename decltype(tag)::type;
-    if constexpr (pipe_plan<PL>()) {
-      using C = pipe::Cfg<PL>;
-      constexpr int TEAMS = PIPE_TEAMS;
-      const void* kern = mode == 0 ? (const void*)k_pipe_fwd<PL, TEAMS> : (const void*)k_pipe_tra<PL, TEAMS>;
-      // at least 120 KB of shared memory: exactly one CTA per SM (each allocates all of TMEM)
-      size_t smem = (size_t)TEAMS * C::team_slots() * sizeof(cplx<T>) + (size_t)(a.nz + 1) * sizeof(int);
-      if (smem < 120 * 1024) smem = 120 * 1024;
-      if (smem > 227 * 1024) return cudaErrorNotSupported;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      int nb = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TEAMS * pipe::TT, smem);
-      if (e != cudaSuccess) return e;
-      if (nb < 1) return cudaErrorCooperativeLaunchTooLarge;
-      PipeArgs args = a;
-      FFTDesc<T> dd = d;
-      void* params[2] = {&args, &dd};
-      return cudaLaunchCooperativeKernel(kern, dim3(sm_count()), dim3(TEAMS * pipe::TT), params, smem, st);
-    } else {
-      return cudaErrorNotSupported;
-    }
-  });
-}
-
-template bool pipe_supported<double>(int, int);
-template bool pipe_supported<float>(int, int);
-template cudaError_t launch_pipe<double>(int, const PipeArgs&, const FFTDesc<double>&, cudaStream_t);
-template cudaError_t launch_pipe<float>(int, const PipeArgs&, const FFTDesc<float>&, cudaStream_t);
 
 template cudaError_t launch_row_r2c<double>(const RowR2CArgs&, const FFTDesc<double>&, int, cudaStream_t);
 template cudaError_t launch_row_r2c<float>(const RowR2CArgs&, const FFTDesc<float>&, int, cudaStream_t);

@@ -33,9 +33,11 @@ def test_version_and_length_family():
     lib = _lib.lib()
     assert b"sm_100a" in lib.bttb_version()
     # smallest supported FFT length >= n: 2^a (a>=3), 2^a*3^b or 2^a*5^b (a>=2, b>=1),
-    # or a power of two with a compile-time plan within 5% of it (2048)
+    # or a power of two with a compile-time plan within 5% of it (2048); above
+    # 8192 the generic-length path: the smallest 2^a 3^b 5^c (at most 65536)
     expect = {1: 8, 3: 8, 9: 12, 11: 12, 13: 16, 49: 64, 79: 80, 99: 100, 335: 384, 419: 432,
-              511: 512, 1999: 2048, 1990: 2048, 1900: 1944, 2049: 2304, 8192: 8192, 8193: -1}
+              511: 512, 1999: 2048, 1990: 2048, 1900: 1944, 2049: 2304, 8192: 8192, 8193: 8640,
+              8599: 8640, 9000: 9000, 16385: 16875, 65536: 65536, 65537: -1}
     for n, L in expect.items():
         assert lib.bttb_fft_length(n) == L, n
 

@@ -3,8 +3,8 @@ available on this GPU pool).
 
 * Guard zones: ``tools/guard_run.py`` under BTTB_GUARD=1 -- 64 KB pattern
   zones around every library buffer and the spectrum cache, NaN canaries
-  around every caller buffer, every entry point and plan family, default
-  kernels and the opt-in fused pipeline.
+  around every caller buffer, every entry point and plan family: default
+  kernels, layer-chunked workspaces and the generic-length path.
 * Determinism: the operator has no atomics in its reductions, so repeated
   products are bit-identical; a shared-memory or mbarrier race shows up as a
   run-to-run difference.
@@ -24,10 +24,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("env", [{}, {"BTTB_PIPE": "1"}], ids=["default", "pipe"])
+@pytest.mark.parametrize("env", [{}, {"BTTB_CHUNK_BYTES": "20000000"}, {"BTTB_GENERIC": "1"}],
+                         ids=["default", "chunked", "generic"])
 def test_guard_sweep(env):
     e = dict(os.environ, BTTB_GUARD="1", **env)
-    args = [] if not env else ["C4", "C5"]
+    args = [] if not env else ["small", "C1", "C4", "C5"]
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "guard_run.py"), *args], env=e,
                        capture_output=True, text=True, timeout=900)
     print(r.stdout[-4000:], r.stderr[-2000:])
