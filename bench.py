@@ -126,19 +126,67 @@ def measured_traffic(cfg, dtype):
     """DRAM bytes per application from the committed ncu capture (profiles/traffic.json:
     dram__bytes_read.sum + dram__bytes_write.sum over one application's launches), or None
     when that capture was taken on different kernel sources than the ones running."""
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    rec, src = profile_record(f"{cfg}_{dtype}")
+    return (rec.get("bytes_per_apply") if rec else None), src
+
+
+def profile_record(key):
+    """A committed per-kernel ncu figure (profiles/traffic.json) for `key`, with
+    its source; the figure is None when it was captured on other kernel sources."""
     try:
-        with open(tpath) as fh:
-            rec = json.load(fh).get(f"{cfg}_{dtype}")
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            rec = json.load(fh).get(key)
     except (OSError, ValueError):
         return None, None
     if not isinstance(rec, dict):
         return None, None
     src = {"profile": rec.get("profile"), "csrc_sha": rec.get("csrc_sha"), "current_csrc_sha": csrc_digest()}
     if rec.get("csrc_sha") != src["current_csrc_sha"]:
-        src["stale"] = True
-        return None, src
-    return rec.get("bytes_per_apply"), src
+        return None, dict(src, stale=True)
+    return rec, src
+
+
+def c5_cgls_variant(dev, steps):
+    """BASELINE configs[4] on one GPU: 64 gravity models on 256x256x32, fp32,
+    10 CGLS iterations (a G*m and a G^T*d each) in the device-resident loop
+    (bttb_cgls), data = G of seeded N(0, 0.1) models.  The 64 models share
+    each layer's spectrum, so per voxel the loop moves few bytes and the
+    column FFTs bind: the roofline fraction is reported
+    against HBM with the FP32-pipe fraction of the column kernels from the
+    committed ncu capture beside it."""
+    import torch
+
+    import paper_1912_06976_b200 as B
+    from oracle import bttb_oracle as O
+
+    og = O.config_grid("C5")
+    grid = B.make_grid(og.sx, og.sy, og.nz, 0, 0, 0, 0, og.dx, og.dy, og.z)
+    batch, iters = O.CONFIGS["C5"][12], 10
+    st = B.build_transform_stack(grid, B.KernelParams.gravity(), dtype="float32", device=dev.index)
+    truth = torch.tensor(np.random.default_rng(1000).normal(0.0, 0.1, (batch, og.n)), dtype=torch.float32,
+                         device=dev)
+    d = B.apply(st, truth, "forward")
+    for _ in range(3):
+        B.cgls(st, d, iters=iters, history=False)
+    torch.cuda.synchronize()
+    reps = max(3, min(steps, 20))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        B.cgls(st, d, iters=iters, history=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    _, hist = B.cgls(st, d, iters=iters)
+    st.close()
+    peak, _ = peaks()
+    napply = 2 * iters + 1
+    rec, src = profile_record("C5_cgls_f32")
+    return {"ms_per_loop": ms, "iterations": iters, "models": batch,
+            "value": batch * og.n * iters / (ms * 1e-3), "unit": "voxels/s (per G*m + G^T*d pair)",
+            "roofline_frac": napply * algorithmic_bytes(og, 4, batch) / (ms * 1e-3) / 1e9 / peak,
+            "fp32_pipe_frac": rec.get("fp32_pipe_frac") if rec else None, "profile_source": src,
+            "residual_drop_median": float(np.median(hist[:, -1] / hist[:, 0]))}
 
 
 def algorithmic_bytes(g, b, batch):
@@ -510,6 +558,24 @@ def run_ours(a):
                "path": ("C ABI host pointers, asynchronous (copies of consecutive calls overlap)" if e2e_async
                         else "pinned host tensors, side-stream copies into two alternating device buffer sets, "
                              "sharded operator (copies of consecutive steps overlap)")}
+        if world == 1:
+            # the unchanged reference call: apply(stack, numpy array, mode) per
+            # product -- pageable host arrays in, a new numpy array out, synchronous
+            # (each call's copies cross PCIe in one direction, so consecutive calls
+            # cannot overlap the way the asynchronous path above does)
+            x_np, d_np = x_pin.numpy()[0].copy(), d_pin.numpy()[0].copy()
+            B.apply(stack, x_np, "forward")
+            B.apply(stack, d_np, "transpose")
+            n_ref = 3
+            t0 = time.perf_counter()
+            for _ in range(n_ref):
+                B.apply(stack, x_np, "forward")
+                B.apply(stack, d_np, "transpose")
+            t_ref = (time.perf_counter() - t0) / n_ref
+            e2e["reference_api"] = {
+                "value": grid.n / t_ref, "ms_per_step": 1e3 * t_ref,
+                "path": "apply(stack, numpy_array, mode) as the reference's callers make it: pageable numpy "
+                        "arrays, synchronous host path (BTTB_HOST_PTR), new output array per call"}
 
     # max over ranks
     vals = torch.tensor([ms, fwd_ms, tra_ms, t_build], device=dev, dtype=torch.float64)
@@ -554,6 +620,9 @@ def run_ours(a):
         variant_out[other] = (y2.reshape(-1, grid.m)[0].double().cpu().numpy(),
                               xt2.reshape(-1, xt2.shape[-1])[0].double().cpu().numpy())
         st2.close()
+
+    if not a.no_variants and cfg == "C4" and world == 1:
+        variants["C5_cgls_f32"] = c5_cgls_variant(dev, a.steps)
 
     if rank != 0:
         if world > 1:

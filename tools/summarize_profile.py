@@ -17,6 +17,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
+sys.path.insert(0, ROOT)
+from bench import csrc_digest  # noqa: E402  (ties the figures to the kernel sources profiled)
 
 
 def per_kernel(path):
@@ -121,7 +123,9 @@ def main(src, tag):
                 lines.append(f"| {nm} | {n} | {m['gpu__time_duration.sum'] / n / 1e3:.1f} | {rd / 1e6:.1f} | "
                              f"{wr / 1e6:.1f} | {m.get('lts__t_bytes.sum', 0.0) / 1e6:.1f} |")
             per_apply = dram / 2
-            traffic[f"C4_{dt}"] = per_apply
+            traffic[f"C4_{dt}"] = {"bytes_per_apply": per_apply, "profile": tag, "csrc_sha": csrc_digest(),
+                                   "how": "ncu dram__bytes_read.sum + dram__bytes_write.sum over one step's "
+                                          "launches (--cache-control none), / 2 applications"}
             lines += ["", f"DRAM bytes per application (step / 2): {per_apply / 1e9:.3f} GB", ""]
     fpath = os.path.join(src, "full_f64_raw.csv")
     if os.path.exists(fpath):
@@ -129,6 +133,19 @@ def main(src, tag):
         for name, vals in full_metrics(fpath):
             lines.append(f"* `{name}`: " + ", ".join(f"{k} {v}" for k, v in vals.items()))
         lines.append("")
+    cpath = os.path.join(src, "full_c5_raw.csv")
+    if os.path.exists(cpath):
+        lines += ["## ncu --set full (C5 CGLS fp32: column kernels of one loop)", ""]
+        fr = []
+        for name, vals in full_metrics(cpath):
+            lines.append(f"* `{name}`: " + ", ".join(f"{k} {v}" for k, v in vals.items()))
+            if "k_col" in name and "FMA pipe %" in vals:
+                fr.append(float(vals["FMA pipe %"].replace(",", "")) / 100.0)
+        if fr:
+            traffic["C5_cgls_f32"] = {"fp32_pipe_frac": sum(fr) / len(fr), "profile": tag, "csrc_sha": csrc_digest(),
+                                      "how": "mean sm__pipe_fma_cycles_active of the captured column kernels"}
+        lines.append("")
+    traffic = {k: v for k, v in traffic.items() if isinstance(v, dict)}
     json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     open(os.path.join(PROF, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
