@@ -1,7 +1,7 @@
 """Import shim: ``import bttb`` resolves to the sm_100a drop-in.
 
 Put ``paper_1912_06976_b200/compat`` first on ``sys.path`` (INTEGRATION.md
-section 3) and unchanged callers of the reference API get the GPU operator:
+section 1) and unchanged callers of the reference API get the GPU operator:
 the hot path (kernel entries, spectrum cache, forward / transpose products),
 the persistence, the harness and the CLI all come from the drop-in.
 

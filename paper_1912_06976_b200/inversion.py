@@ -55,8 +55,10 @@ def cgls(stack, d, iters=10, damp=0.0, stream=None, history=True):
         if da.ndim not in (1, 2) or da.shape[-1] != g.m:
             raise ValueError(f"{msg}, got shape {da.shape}")
         batch = 1 if da.ndim == 1 else da.shape[0]
-        din = np.ascontiguousarray(da, dtype=stack.dtype)
-        out = np.empty(da.shape[:-1] + (stack.n_local,), dtype=stack.dtype)
+        from .multiply import _host_in, _host_out  # pinned host buffers for the copy engines
+
+        din = _host_in(da, stack.dtype)
+        out = _host_out(da.shape[:-1] + (stack.n_local,), stack.dtype)
         xp, yp, where, sp = din.ctypes.data, out.ctypes.data, _lib.HOST_PTR, 0
         shape = da.shape[:-1]
     hist = np.empty((batch, int(iters) + 1), dtype=np.float64) if history else None
