@@ -34,7 +34,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
@@ -298,8 +298,9 @@ def run_reference(a):
     C4): the reference algorithm (pinned oracle port -- the reference is pure
     numpy) with its two complex128 spectrum stacks built once, then per step
     one forward and one transpose over all layers, layers threaded over the
-    host cores.  Steps are capped at 10 and warm-up at 1 so the run stays
-    within a few minutes (each C4 step is ~7 s of 16-thread CPU work)."""
+    host cores.  The driver's K and W are honoured (capped at 30 steps and 5
+    warm-up steps: each C4 step is ~7 s of 16-thread CPU work, so K=20, W=5
+    is ~3 minutes)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -312,8 +313,8 @@ def run_reference(a):
     g = O.config_grid(a.config)
     kind, consts = O.config_kernel(a.config)
     x, d = O.make_inputs(a.config, g, batch=1)
-    steps = max(1, min(a.steps, 10))
-    warm = max(0, min(a.warmup, 1))
+    steps = max(1, min(a.steps, 30))
+    warm = max(0, min(a.warmup, 5))
     with ThreadPoolExecutor(cores) as pool:
         t0 = time.perf_counter()
         fw, tr = O.build_spectra_threaded(g, kind, consts, list(range(g.nz)), pool)
