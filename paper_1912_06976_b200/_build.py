@@ -24,6 +24,7 @@ UNITS = {
     "spectral.cu": ["-Xptxas", "-v"] if os.environ.get("BTTB_PTXAS_VERBOSE") else [],
     "cgls.cu": [],
     "generic.cu": [],
+    "hoststage.cu": [],
     "capi.cu": [],
 }
 

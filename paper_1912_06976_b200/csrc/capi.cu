@@ -20,6 +20,7 @@
 #include "cgls.h"
 #include "entries.h"
 #include "generic.h"
+#include "hoststage.h"
 #include "spectral.h"
 
 using namespace bttb;
@@ -334,6 +335,7 @@ struct bttb_plan_s {
   GenericCtx gen;
   double2* gen_tw[2] = {nullptr, nullptr};
   DevBuf work, hin, hout;
+  HostStage hstage;  // pinned chunk ring for pageable host buffers (BTTB_HOST_PTR)
   DevBuf cg, cg_hist;  // CGLS driver workspace and residual history (bttb_cgls)
   cudaStream_t stream = nullptr;   // internal stream the products run on
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -725,6 +727,7 @@ void destroy_plan(bttb_plan_s* p) {
   DeviceGuard g(p->device);
   if (p->spectra) guard_free(p->spectra);
   generic_release(p);
+  p->hstage.release();
   p->fx.release();
   p->fy.release();
   p->work.release();
@@ -1048,7 +1051,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   if (where == BTTB_HOST_PTR) {
     int rc;
     if ((rc = p->hin.ensure(in_elems * esz)) || (rc = p->hout.ensure(out_elems * esz))) return rc;
-    CU(cudaMemcpyAsync(p->hin.p, x, in_elems * esz, cudaMemcpyHostToDevice, st));
+    CU(stage_h2d(p->hstage, p->hin.p, x, in_elems * esz, st));
     xd = p->hin.p;
     yd = p->hout.p;
   } else if (where != BTTB_DEVICE_PTR) {
@@ -1064,10 +1067,7 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   if (rc) return rc;
   CU(cudaEventRecord(p->ev_out, p->stream));
   CU(cudaStreamWaitEvent(st, p->ev_out, 0));
-  if (where == BTTB_HOST_PTR) {
-    CU(cudaMemcpyAsync(y, yd, out_elems * esz, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-  }
+  if (where == BTTB_HOST_PTR) CU(stage_d2h(p->hstage, y, yd, out_elems * esz, st));
   return BTTB_OK;
 }
 
@@ -1093,7 +1093,7 @@ int bttb_cgls(bttb_plan* p, const void* d, void* m_out, int64_t batch, int iters
   int rc;
   if (where == BTTB_HOST_PTR) {
     if ((rc = p->hin.ensure(dbytes)) || (rc = p->hout.ensure(mbytes))) return rc;
-    CU(cudaMemcpyAsync(p->hin.p, d, dbytes, cudaMemcpyHostToDevice, st));
+    CU(stage_h2d(p->hstage, p->hin.p, d, dbytes, st));
     dd = p->hin.p;
     md = p->hout.p;
   }
@@ -1113,11 +1113,11 @@ int bttb_cgls(bttb_plan* p, const void* d, void* m_out, int64_t batch, int iters
   if (rc) return rc;
   CU(cudaEventRecord(p->ev_out, p->stream));
   CU(cudaStreamWaitEvent(st, p->ev_out, 0));
-  if (where == BTTB_HOST_PTR) CU(cudaMemcpyAsync(m_out, md, mbytes, cudaMemcpyDeviceToHost, st));
   if (resid_norms) {
     CU(cudaMemcpyAsync(resid_norms, hist, sizeof(double) * batch * (iters + 1), cudaMemcpyDeviceToHost, st));
   }
-  if (where == BTTB_HOST_PTR || resid_norms) CU(cudaStreamSynchronize(st));
+  if (where == BTTB_HOST_PTR) CU(stage_d2h(p->hstage, m_out, md, mbytes, st));
+  if (resid_norms) CU(cudaStreamSynchronize(st));
   return BTTB_OK;
 }
 

@@ -6,34 +6,21 @@ array (x is never mutated).  Extensions: a leading batch axis, and CUDA torch
 tensors in/out (zero-copy device pointers on the current stream) for
 device-resident iterative use.
 """
-import os
-
 import numpy as np
 
 from . import _lib
 
 __all__ = ["apply", "relative_error"]
 
-# Host buffers of the numpy path.  The DMA engines read and write page-locked
-# memory at the PCIe rate, but a pageable source goes through the driver's
-# single-threaded staging (C4 model, 1.03 GB: 89 ms) and a freshly allocated
-# pageable destination page-faults under the copy (203 ms); on a B200 box a
-# pinned destination takes 18 ms (tools/hostcopy_probe.py).  So large outputs
-# are allocated in pinned memory (torch's caching host allocator: the pages
-# are reused across calls and stay alive as long as the returned array) and
-# large inputs are copied into pinned memory by several threads first.
+# Host buffers of the numpy path.  A freshly allocated pageable destination
+# page-faults under the device-to-host copy (C4 model, 1.03 GB: 203 ms on a
+# B200 box, vs 18 ms into pinned memory -- tools/hostcopy_probe.py), so large
+# outputs are allocated in pinned memory (torch's caching host allocator: the
+# pages are reused across calls and live as long as the returned array).
+# Large pageable INPUTS are handled by the library (csrc/hoststage.cu:
+# chunked staging through a pinned ring by a pool of host threads, overlapped
+# with the copy engine).
 _PINNED_MIN = 1 << 22
-_WORKERS = max(1, min(8, os.cpu_count() or 1))
-_POOL = None
-
-
-def _pool():
-    global _POOL
-    if _POOL is None:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _POOL = ThreadPoolExecutor(_WORKERS)
-    return _POOL
 
 
 def _pinned_empty(shape, dt):
@@ -43,23 +30,14 @@ def _pinned_empty(shape, dt):
         if not torch.cuda.is_available():
             raise RuntimeError
         t = torch.empty(tuple(shape), dtype=torch.float64 if dt == np.float64 else torch.float32, pin_memory=True)
-    except Exception:  # no torch / no CUDA runtime: the driver stages pageable memory itself
+    except Exception:  # no torch / no CUDA runtime: the library stages the copy itself
         return np.empty(shape, dtype=dt)
     return t.numpy()
 
 
 def _host_in(xa, dt):
-    """x as a contiguous `dt` array the copy engines read at full rate."""
-    if xa.nbytes < _PINNED_MIN:
-        return np.ascontiguousarray(xa, dtype=dt)
-    buf = _pinned_empty(xa.shape, dt)
-    src, dst = xa.reshape(-1), buf.reshape(-1)
-    n = dst.size
-    k = 4 * _WORKERS
-    bounds = [n * i // k for i in range(k + 1)]
-    list(_pool().map(lambda i: np.copyto(dst[bounds[i]:bounds[i + 1]], src[bounds[i]:bounds[i + 1]],
-                                         casting="unsafe"), range(k)))
-    return buf
+    """x as a contiguous `dt` array (the library stages pageable memory)."""
+    return np.ascontiguousarray(xa, dtype=dt)
 
 
 def _host_out(shape, dt):
