@@ -26,6 +26,10 @@ ncu --profile-from-start off --set full --import-source on --cache-control none 
     -o $OUT/full_f64 python bench.py --profile-step --no-cpu-baseline --no-variants --no-e2e > $OUT/ncu3.log 2>&1
 ncu -i $OUT/full_f64.ncu-rep --page raw --csv > $OUT/full_f64_raw.csv 2>/dev/null
 ncu -i $OUT/full_f64.ncu-rep --page details --csv > $OUT/full_f64_details.csv 2>/dev/null
+ncu --profile-from-start off --set full --cache-control none --clock-control none \
+    -k regex:"k_row_r2c_t2d|k_row_c2r_mirror" -c 4 -o $OUT/full_f32 python bench.py --dtype f32 --profile-step --no-cpu-baseline --no-variants --no-e2e > $OUT/ncu5.log 2>&1
+ncu -i $OUT/full_f32.ncu-rep --page raw --csv > $OUT/full_f32_raw.csv 2>/dev/null
+rm -f $OUT/full_f32.ncu-rep
 ncu --profile-from-start off --set full --import-source on --cache-control none --clock-control none \
     -k regex:"k_col" -c 4 -o $OUT/full_c5 python bench.py --config C5 --dtype f32 --cgls 10 --profile-step > $OUT/ncu4.log 2>&1
 ncu -i $OUT/full_c5.ncu-rep --page raw --csv > $OUT/full_c5_raw.csv 2>/dev/null

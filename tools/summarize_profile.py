@@ -133,6 +133,12 @@ def main(src, tag):
         for name, vals in full_metrics(fpath):
             lines.append(f"* `{name}`: " + ", ".join(f"{k} {v}" for k, v in vals.items()))
         lines.append("")
+    f32path = os.path.join(src, "full_f32_raw.csv")
+    if os.path.exists(f32path):
+        lines += ["## ncu --set full (fp32 row kernels of one C4 step)", ""]
+        for name, vals in full_metrics(f32path):
+            lines.append(f"* `{name}`: " + ", ".join(f"{k} {v}" for k, v in vals.items()))
+        lines.append("")
     cpath = os.path.join(src, "full_c5_raw.csv")
     if os.path.exists(cpath):
         lines += ["## ncu --set full (C5 CGLS fp32: column kernels of one loop)", ""]
