@@ -83,7 +83,7 @@ def main(src, tag):
     ref = last_json(os.path.join(src, "bench_ref.json"))
     if bench:
         shutil.copy(os.path.join(src, "bench.json"), os.path.join(PROF, f"{tag}_bench.json"))
-        lines += ["## bench.py (default: C4 fp64, 100 steps)", "",
+        lines += ["## bench.py (default: C4 fp64, 20 steps)", "",
                   f"* value {bench['value']:.4g} voxels/s, {bench['ms_per_step']:.3f} ms/step, "
                   f"roofline frac {bench['roofline']['frac']:.3f} of {bench['roofline']['peak']} GB/s, "
                   f"clocks {bench.get('clocks')}",
