@@ -268,3 +268,36 @@ def test_pageable_host_buffers_staged_copies():
         xd = B.apply(st, torch.tensor(v, device="cuda"), "transpose").cpu().numpy()
     np.testing.assert_array_equal(y, yd)
     np.testing.assert_array_equal(xt, xd)
+
+
+def test_concurrent_numpy_applies_with_staged_copies():
+    """apply is reentrant and thread-safe (the reference's contract,
+    pkg/README.md:120-122): four threads on one plan and one on a second plan,
+    with pageable inputs above the 16 MB staging threshold (the shared host
+    copy pool and the per-plan pinned rings), give the single-threaded results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    og = O.config_grid("C4")
+    params = B.KernelParams.magnetic(*O.CONFIGS["C4"][11])
+    grid = B.make_grid(og.sx, og.sy, og.nz, og.pxl, og.pxr, og.pyl, og.pyr, og.dx, og.dy, og.z)
+    rng = np.random.default_rng(41)
+    with B.build_transform_stack(grid, params, layers=(10, 13)) as s1, \
+            B.build_transform_stack(grid, params, layers=(60, 63)) as s2:
+        xs = [rng.uniform(0.0, 0.05, s1.n_local) for _ in range(5)]
+        want = [B.apply(s1 if i < 4 else s2, x, "forward") for i, x in enumerate(xs)]
+        vs = [rng.normal(size=og.m) for _ in range(5)]
+        want_t = [B.apply(s1 if i < 4 else s2, v, "transpose") for i, v in enumerate(vs)]
+
+        def job(i):
+            st = s1 if i < 4 else s2
+            out = []
+            for _ in range(3):
+                out.append((B.apply(st, xs[i], "forward"), B.apply(st, vs[i], "transpose")))
+            return out
+
+        with ThreadPoolExecutor(5) as pool:
+            results = list(pool.map(job, range(5)))
+    for i, res in enumerate(results):
+        for f, t in res:
+            np.testing.assert_array_equal(f, want[i])
+            np.testing.assert_array_equal(t, want_t[i])
