@@ -195,17 +195,66 @@ def algorithmic_bytes(g, b, batch):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an NVML thread reads them every ~5 ms (the timed region of a
+    20-step C4 run is only ~70 ms, too short for nvidia-smi's 50 ms loop and
+    its start-up); only samples after mark() -- the start of the timed
+    region -- count.  Falls back to an nvidia-smi loop without NVML."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.thread = None
+        self.samples = []
+        self.t_mark = None
+        self.max_mhz = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        props = torch.cuda.get_device_properties(self.index)
+        bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        try:
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
+        import threading
+
+        try:
+            nv, h = self._nvml_handle()
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            self._start_smi()
+            return
+        self._stop = False
+
+        def loop():
+            while not self._stop:
+                try:
+                    mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((time.perf_counter(), mhz, [n for n, b in bits.items() if rs & b]))
+                except Exception:
+                    pass
+                time.sleep(0.005)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+
+    def _start_smi(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -214,13 +263,24 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def mark(self):
+        """The timed region starts now."""
+        self.t_mark = time.perf_counter()
+
     def stop(self):
+        if self.thread is not None:
+            self._stop = True
+            self.thread.join(timeout=2)
+            rows = [(m, r) for (tt, m, r) in self.samples if self.t_mark is None or tt >= self.t_mark]
+            sm = [m for m, _ in rows]
+            reasons = sorted({n for _, r in rows for n in r})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                    "samples": len(sm), "reasons": reasons, "source": "nvml, 5 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
         rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 6]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         sm, mx = [], None
         for r in rows:
@@ -229,11 +289,11 @@ class ClockSampler:
                 mx = float(r[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, r[3:7]):
+            for nm, v in zip(self.NAMES, r[3:7]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi, 50 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -449,6 +509,7 @@ def run_ours(a):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    sampler.mark()
     e0.record(stream)
     for _ in range(a.steps):
         run()
@@ -822,6 +883,7 @@ def run_cgls(a):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    sampler.mark()
     e0.record(stream)
     for _ in range(a.steps):
         run()
