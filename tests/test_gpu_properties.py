@@ -301,3 +301,29 @@ def test_concurrent_numpy_applies_with_staged_copies():
         for f, t in res:
             np.testing.assert_array_equal(f, want[i])
             np.testing.assert_array_equal(t, want_t[i])
+
+
+def test_pageable_staging_odd_sizes():
+    """Staged pageable copies with byte counts that are not multiples of the
+    32 MB chunk, of the 64-byte thread split or of 16 (fp32, odd row lengths):
+    1001 x 1003 stations over 3 (fp64, 24.1 MB) and 5 (fp32, 20.1 MB) layers."""
+    import torch
+
+    from paper_1912_06976_b200.multiply import apply_into
+
+    for dtype, nz in (("float64", 3), ("float32", 5)):
+        og = O.ogrid(1001, 1003, nz, 0, 0, 0, 0, 20.0, 20.0, [20.0 * r for r in range(nz + 1)])
+        grid = B.make_grid(og.sx, og.sy, og.nz, 0, 0, 0, 0, og.dx, og.dy, og.z)
+        npdt = np.float64 if dtype == "float64" else np.float32
+        rng = np.random.default_rng(43)
+        with B.build_transform_stack(grid, B.KernelParams.gravity(), dtype=dtype) as st:
+            x = rng.uniform(0.0, 1.0, og.n).astype(npdt)
+            v = rng.normal(size=og.m).astype(npdt)
+            y = np.empty(og.m, dtype=npdt)
+            xt = np.empty(og.n, dtype=npdt)
+            apply_into(st, "forward", x.ctypes.data, y.ctypes.data, 1, host=True)
+            apply_into(st, "transpose", v.ctypes.data, xt.ctypes.data, 1, host=True)
+            yd = B.apply(st, torch.tensor(x, device="cuda"), "forward").cpu().numpy()
+            xd = B.apply(st, torch.tensor(v, device="cuda"), "transpose").cpu().numpy()
+        np.testing.assert_array_equal(y, yd)
+        np.testing.assert_array_equal(xt, xd)
