@@ -583,8 +583,8 @@ template <class PL> struct RowTile {
   static constexpr int BOXK = HX < kBoxKx ? HX : kBoxKx;  // box extent along kx (the tensor map's)
   static constexpr int NBOX = (HX + BOXK - 1) / BOXK;
   static constexpr int PER = 128 / (int)sizeof(cplx<typename PL::Scalar>);
-  // kx extent of one staged row when the two rows arrive as separate boxes,
-  // rounded so the second row's tile starts 128-byte aligned
+  // kx extent of the staged boxes, rounded to 128 bytes (the [kx][2 rows]
+  // tile holds 2 * SPAN complex values)
   static constexpr int SPAN = (NBOX * BOXK + PER - 1) / PER * PER;
   // shared slots (complex) of one team: exchange buffer or staged box, whichever
   // is larger, rounded to 128 bytes (tensor-TMA shared addresses are 128-B aligned)
@@ -736,18 +736,14 @@ __global__ void __launch_bounds__(MAXT, MINB)
 // The FFT input is read straight from the staged tile: element n of the
 // packed row pair is z[n] = A[n] + i B[n] (n <= L/2) or conj(A[L-n]) +
 // i conj(B[L-n]) (Hermitian half), so no intermediate exchange-buffer pass.
-// SPLIT (fp64): each row arrives as its own [kx] box (16-byte box rows), so
-// A and B are contiguous arrays and every tile read is conflict-free.
-template <class PL, int MAXT, int MINB, int TEAMS, bool QUAD = false, bool SPLIT = false>
+template <class PL, int MAXT, int MINB, int TEAMS, bool QUAD = false>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_row_c2r_t2d(RowC2RArgs a, FFTDesc<typename PL::Scalar> d, const __grid_constant__ CUtensorMap imap) {
   static_assert(!QUAD || TEAMS == 2, "a four-row box takes two teams");
-  static_assert(!(QUAD && SPLIT), "split row boxes are per team");
   using T = typename PL::Scalar;
   using V = cplx<T>;
   using RT = RowTile<PL>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L, HX = RT::HX, NBOX = RT::NBOX;
-  constexpr int SPAN = RT::SPAN;  // kx extent of one staged row (split boxes)
   extern __shared__ __align__(16) unsigned char smraw[];
   const int tslots = RT::slots((PL::slots(L) + 1) & ~1);
   const int c = TEAMS > 1 ? threadIdx.x / NT : 0;
@@ -779,26 +775,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
       fence_mbar_init();
       // every box delivers its full extent (out-of-range rows zero-filled)
       mbar_arrive_expect_tx(bar, (uint32_t)(NBOX * RT::BOXK * 2 * sizeof(V)));
-      for (int b = 0; b < NBOX; ++b) {
-        if constexpr (SPLIT) {
-          tma_load_3d(sm + b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
-          tma_load_3d(sm + SPAN + b * RT::BOXK, &imap, 2 * jb, b * RT::BOXK, s, bar);
-        } else {
-          tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
-        }
-      }
+      for (int b = 0; b < NBOX; ++b) tma_load_3d(sm + 2 * b * RT::BOXK, &imap, 2 * ja, b * RT::BOXK, s, bar);
     }
     __syncthreads();
     if (active) mbar_wait(bar, 0);
-    if constexpr (SPLIT) {
-      sA = sm;
-      sB = sm + SPAN;
-      st = 1;
-    } else {
-      sA = sm;
-      sB = sm + 1;
-      st = 2;
-    }
+    sA = sm;
+    sB = sm + 1;
+    st = 2;
   }
   V v[E];
 #pragma unroll
@@ -1073,7 +1056,6 @@ template <class PL> struct Shape {
   static constexpr int tra_regs =
       (sizeof(T) == 8 && PL::E <= 16 && col_regs_rounded > TRA_REGS_F64) ? TRA_REGS_F64 : col_regs_rounded;
   static constexpr int tra_minb = PL::kStatic ? minb(col_threads, tra_regs) : 1;
-  static constexpr int rowtma_minb = PL::kStatic ? minb(NT, 128) : 1;
   static constexpr int t2d_teams = T2D_TEAMS;
   static constexpr int t2d_minb = PL::kStatic ? minb(T2D_TEAMS * NT, row_regs) : 1;
   static constexpr int quad_minb = PL::kStatic ? minb(2 * NT, row_regs) : 1;
@@ -1320,9 +1302,8 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
           return cudaGetLastError();
         }
       }
-      constexpr bool SPLIT = false;
       if (t2d_ok() &&
-          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, SPLIT ? 1 : 2)) {
+          encode_rowpair_map<T>(&imap, a.in, a.nrows, a.Hx, a.nslabs, a.ld_in, a.in_sstride, 2)) {
         constexpr int TM = Shape<PL>::t2d_teams;
         if constexpr (PL::kR16x16x8 && PL::kPerPass) {
           if (a.tw_816 && c2r_mirror_ok()) {
@@ -1337,7 +1318,7 @@ cudaError_t launch_row_c2r(const RowC2RArgs& a, const FFTDesc<T>& d, int E, cuda
             return cudaGetLastError();
           }
         }
-        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM, false, SPLIT>;
+        auto kern = k_row_c2r_t2d<PL, TM * PL::NT, Shape<PL>::t2d_minb, TM, false>;
         const size_t smem = (size_t)TM * RowTile<PL>::slots((PL::slots(d.L) + 1) & ~1) * sizeof(cplx<T>) + 16 * TM;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
