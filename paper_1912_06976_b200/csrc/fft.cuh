@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <type_traits>
 
+#include "tma.cuh"
+
 namespace bttb {
 
 template <class T> struct CT;
@@ -334,11 +336,96 @@ __device__ __forceinline__ void gen_twiddles(V (&w)[R], const V* __restrict__ tw
   });
 }
 
-template <class T, int E, int R, int NS, int NT, int L, bool PP = false>
-__device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw) {
+// ---------------------------------------------------------------------------
+// Loop-invariant pass twiddles in tensor memory.  A column-stage CTA runs the
+// SAME compile-time plan with the same thread index for every depth layer, so
+// the R-1 twiddles of each of its butterfly blocks never change: they are
+// computed once per CTA (exactly as the passes below would compute them, so
+// the products are bit-identical) and parked in the thread's TMEM lane.  Each
+// pass then fetches them with tcgen05.ld -- no L1 wavefronts (the table
+// loads), no FP64 twiddle products (the generation) -- at the cost of 64-128
+// TMEM columns per CTA, which this workload otherwise leaves idle.
+// Layout: pass p (NS > 1) block b at column TOFF_p + b * tw_cols<V, R_p>,
+// complex w^r at (r-1)*sizeof(V)/4; chunks of 16 columns (tcgen05 x16).
+// ---------------------------------------------------------------------------
+template <class V, int R> __host__ __device__ constexpr int tw_cols() {
+  return ((int)(sizeof(V) / 4) * (R - 1) + 15) / 16 * 16;
+}
+struct NoTwCache {
+  static constexpr bool on = false;
+  uint32_t ta = 0;
+};
+struct TmemTwCache {  // ta = TMEM address of this thread's lane, column 0 of the cache
+  static constexpr bool on = true;
+  uint32_t ta;
+};
+__device__ __forceinline__ void tw_pack(double2 a, uint32_t* r) {
+  r[0] = (uint32_t)__double2loint(a.x);
+  r[1] = (uint32_t)__double2hiint(a.x);
+  r[2] = (uint32_t)__double2loint(a.y);
+  r[3] = (uint32_t)__double2hiint(a.y);
+}
+__device__ __forceinline__ void tw_pack(float2 a, uint32_t* r) {
+  r[0] = __float_as_uint(a.x);
+  r[1] = __float_as_uint(a.y);
+}
+__device__ __forceinline__ void tw_unpack(const uint32_t* r, double2& a) {
+  a = make_double2(__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2]));
+}
+__device__ __forceinline__ void tw_unpack(const uint32_t* r, float2& a) {
+  a = make_float2(__uint_as_float(r[0]), __uint_as_float(r[1]));
+}
+template <class V, int R, int COL>
+__device__ __forceinline__ void tw_store(uint32_t ta, const V (&w)[R]) {
+  constexpr int N = tw_cols<V, R>(), CPC = sizeof(V) / 4;
+  uint32_t u[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) u[i] = 0u;
+  sfor<1, R>([&](auto rc) { constexpr int r = decltype(rc)::value; tw_pack(w[r], u + (r - 1) * CPC); });
+  sfor<0, N / 16>([&](auto gc) {
+    constexpr int g = decltype(gc)::value;
+    uint32_t c[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = u[16 * g + i];
+    tmem_st16(ta + COL + 16 * g, c);
+  });
+}
+template <class V, int R, int COL>
+__device__ __forceinline__ void tw_load(uint32_t ta, V (&w)[R]) {
+  constexpr int N = tw_cols<V, R>(), CPC = sizeof(V) / 4;
+  uint32_t u[N];
+  sfor<0, N / 16>([&](auto gc) {
+    constexpr int g = decltype(gc)::value;
+    uint32_t c[16];
+    tmem_ld16(ta + COL + 16 * g, c);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) u[16 * g + i] = c[i];
+  });
+  tmem_wait_ld();
+  sfor<1, R>([&](auto rc) { constexpr int r = decltype(rc)::value; tw_unpack(u + (r - 1) * CPC, w[r]); });
+}
+
+template <class T, int E, int R, int NS, int NT, int L, bool PP = false, int TOFF = 0, class TwC = NoTwCache>
+__device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw,
+                                              const TwC& tc = TwC{}) {
   using V = cplx<T>;
   constexpr int NB = E / R;
   constexpr int STRIDE = L / (NS * R);
+  if constexpr (TwC::on && PP && NS > 1) {
+    sfor<0, NB>([&](auto bc) {
+      constexpr int b = decltype(bc)::value;
+      V u[R], w[R];
+      sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; u[r] = v[b + r * NB]; });
+      tw_load<V, R, TOFF + b * tw_cols<V, R>()>(tc.ta, w);
+      sfor<1, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        u[r] = cmul(u[r], w[r]);
+      });
+      dft<R>(u);
+      sfor<0, R>([&](auto rc) { constexpr int r = decltype(rc)::value; v[b + r * NB] = u[r]; });
+    });
+    return;
+  }
   constexpr bool GEN = (sizeof(T) == 8 ? BTTB_TWGEN : BTTB_TWGEN_F32) && PP && NS > 1 && R >= 4;
   // When a thread's blocks b sit at k = t + NT*b (NT*NB <= NS), the twiddle
   // w^(r*k) of block b is block 0's times the constant w_Q^(r*b), Q = NS*R/NT:
@@ -396,6 +483,71 @@ __device__ __forceinline__ void spass_compute(cplx<T> (&v)[E], int t, const cplx
   });
 }
 
+// The twiddles spass_compute (no cache) multiplies block b of pass (NS, R)
+// by, computed the same way; stored to the TMEM cache.
+template <class T, int E, int R, int NS, int NT, int L, int TOFF>
+__device__ __forceinline__ void spass_tw_fill(int t, const cplx<T>* __restrict__ tw, uint32_t ta) {
+  using V = cplx<T>;
+  constexpr int NB = E / R;
+  constexpr bool GEN = (sizeof(T) == 8 ? BTTB_TWGEN : BTTB_TWGEN_F32) && NS > 1 && R >= 4;
+  constexpr bool DERIVE = NS > 1 && NB > 1 && NT * NB <= NS && (NS * R) % NT == 0 && has_twr((NS * R) / NT);
+  if constexpr (NS > 1) {
+    if constexpr (DERIVE) {
+      constexpr int Q = (NS * R) / NT;
+      V w0[R];
+      if constexpr (GEN) {
+        gen_twiddles<V, R, NS>(w0, tw, t);
+      } else {
+        sfor<1, R>([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
+          w0[r] = __ldg(&tw[(r - 1) * NS + t]);
+        });
+      }
+      sfor<0, NB>([&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        V w[R];
+        sfor<1, R>([&](auto rc) {
+          constexpr int r = decltype(rc)::value;
+          w[r] = b == 0 ? w0[r] : twc<Q, (r * b) % Q>(w0[r]);
+        });
+        tw_store<V, R, TOFF + b * tw_cols<V, R>()>(ta, w);
+      });
+    } else {
+      sfor<0, NB>([&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        const int k = (t + NT * b) % NS;
+        V w[R];
+        if constexpr (GEN) {
+          gen_twiddles<V, R, NS>(w, tw, k);
+        } else {
+          sfor<1, R>([&](auto rc) {
+            constexpr int r = decltype(rc)::value;
+            w[r] = __ldg(&tw[(r - 1) * NS + k]);
+          });
+        }
+        tw_store<V, R, TOFF + b * tw_cols<V, R>()>(ta, w);
+      });
+    }
+  }
+}
+
+template <class T, int E, int L, int OFF, int NS, int TOFF, int R, int... Rest>
+__device__ __forceinline__ void sfft_tw_fill(int t, const cplx<T>* __restrict__ tw, uint32_t ta) {
+  constexpr int NT = L / E;
+  spass_tw_fill<T, E, R, NS, NT, L, TOFF>(t, tw + OFF, ta);
+  if constexpr (sizeof...(Rest) > 0)
+    sfft_tw_fill<T, E, L, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R,
+                 (NS > 1 ? TOFF + (E / R) * tw_cols<cplx<T>, R>() : TOFF), Rest...>(t, tw, ta);
+}
+// TMEM columns of a plan's twiddle cache
+template <class V, int E, int NS, int R, int... Rest> __host__ __device__ constexpr int sfft_tw_cols() {
+  constexpr int here = NS > 1 ? (E / R) * tw_cols<V, R>() : 0;
+  if constexpr (sizeof...(Rest) > 0)
+    return here + sfft_tw_cols<V, E, NS * R, Rest...>();
+  else
+    return here;
+}
+
 template <class T, int E, int R, int NS, int NT, int PAD>
 __device__ __forceinline__ void spass_store(const cplx<T> (&v)[E], cplx<T>* sm, int t, bool active = true) {
   constexpr int NB = E / R;
@@ -433,13 +585,13 @@ struct TeamSync {
 // asynchronous copy that still reads the exchange buffer)
 // PP: tw is the per-pass table block (OFF = this pass's offset in it);
 // otherwise tw is the length-L table.
-template <class T, int E, int L, int PAD, bool PP, int OFF, int NS, int R, int... Rest, class Hook = NoHook,
-          class Sync = CtaSync>
-__device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
-                                     bool active = true, Hook hook = Hook{}, Sync sync = Sync{}) {
+template <class T, int E, int L, int PAD, bool PP, int OFF, int NS, int TOFF, class TwC, int R, int... Rest,
+          class Hook = NoHook, class Sync = CtaSync>
+__device__ __forceinline__ void sfft_c(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
+                                       const TwC& tc, bool active = true, Hook hook = Hook{}, Sync sync = Sync{}) {
   constexpr int NT = L / E;
   static_assert(E % R == 0, "radix must divide elements per thread");
-  spass_compute<T, E, R, NS, NT, L, PP>(v, active ? t : 0, PP ? tw + OFF : tw);
+  spass_compute<T, E, R, NS, NT, L, PP, TOFF, TwC>(v, active ? t : 0, PP ? tw + OFF : tw, tc);
   if constexpr (sizeof...(Rest) > 0) {
     if constexpr (NS == 1) hook();
     sync();
@@ -448,9 +600,17 @@ __device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const 
 #pragma unroll
     for (int s = 0; s < E; ++s)
       if (active) v[s] = sm[pad_slot<PAD>(t + NT * s)];
-    sfft<T, E, L, PAD, PP, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R, Rest...>(v, sm, t, tw, active, NoHook{},
-                                                                                  sync);
+    sfft_c<T, E, L, PAD, PP, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R,
+           (NS > 1 ? TOFF + (E / R) * tw_cols<cplx<T>, R>() : TOFF), TwC, Rest...>(v, sm, t, tw, tc, active,
+                                                                                  NoHook{}, sync);
   }
+}
+
+template <class T, int E, int L, int PAD, bool PP, int OFF, int NS, int R, int... Rest, class Hook = NoHook,
+          class Sync = CtaSync>
+__device__ __forceinline__ void sfft(cplx<T> (&v)[E], cplx<T>* sm, int t, const cplx<T>* __restrict__ tw,
+                                     bool active = true, Hook hook = Hook{}, Sync sync = Sync{}) {
+  sfft_c<T, E, L, PAD, PP, OFF, NS, 0, NoTwCache, R, Rest...>(v, sm, t, tw, NoTwCache{}, active, hook, sync);
 }
 
 // Plan concepts used by the kernels: Scalar, E, nt(d), slot(e), slots(L),
@@ -494,6 +654,15 @@ struct SPlanT {
   __device__ __forceinline__ static void fft_hook(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
                                                   Hook hook) {
     sfft<T, E_, L, PAD, PP, 0, 1, Rs...>(v, sm, t, table(d), true, hook);
+  }
+  // twiddle cache in TMEM (PP plans): columns, fill once per CTA, transforms that use it
+  static constexpr int kTwCols = sfft_tw_cols<cplx<T>, E_, 1, Rs...>();
+  __device__ __forceinline__ static void tw_fill(int t, const FFTDesc<T>& d, uint32_t ta) {
+    sfft_tw_fill<T, E_, L, 0, 1, 0, Rs...>(t, table(d), ta);
+  }
+  __device__ __forceinline__ static void fft_tc(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,
+                                                TmemTwCache tc) {
+    sfft_c<T, E_, L, PAD, PP, 0, 1, 0, TmemTwCache, Rs...>(v, sm, t, table(d), tc);
   }
   // one team of a multi-team CTA: exchanges synchronise on the team's barrier
   __device__ __forceinline__ static void fft_team(cplx<T> (&v)[E_], cplx<T>* sm, int t, const FFTDesc<T>& d,

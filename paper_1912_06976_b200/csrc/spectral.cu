@@ -291,8 +291,49 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra(ColTraArgs a, FFTDesc<ty
 // costs no registers.  Spectra are fetched with an L2 evict-first policy.
 // Shared layout: [exchange Ls][spectrum L][Y or D column nv][2 mbarriers].
 // ---------------------------------------------------------------------------
-template <class PL, int MAXT, int MINB>
+// TWC: the plan's pass twiddles live in a per-CTA TMEM cache (fft.cuh,
+// TmemTwCache), filled once and reused for every layer.
+template <class PL, bool TWC> struct TwCache {
+  static constexpr int cols = TWC ? PL::kTwCols : 0;
+  static constexpr int ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  __device__ __forceinline__ static TmemTwCache setup(uint32_t* taddr_s, int t, const FFTDesc<typename PL::Scalar>& d) {
+    TmemTwCache tc{0u};
+    if constexpr (TWC) {
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+      tc.ta = *taddr_s + ((uint32_t)(32 * ((t / 32) & 3)) << 16);
+      PL::tw_fill(t, d, tc.ta);
+      tmem_wait_st();
+    }
+    return tc;
+  }
+  __device__ __forceinline__ static void alloc(uint32_t* taddr_s, int t) {
+    if constexpr (TWC) {
+      if (t < 32) tmem_alloc<ncols>(taddr_s);
+    }
+  }
+  __device__ __forceinline__ static void release(uint32_t* taddr_s, int t) {
+    if constexpr (TWC) {
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+      if (t < 32) tmem_dealloc<ncols>(*taddr_s);
+    }
+  }
+  template <int E>
+  __device__ __forceinline__ static void fft(cplx<typename PL::Scalar> (&v)[E], cplx<typename PL::Scalar>* sm, int t,
+                                             const FFTDesc<typename PL::Scalar>& d, TmemTwCache tc) {
+    if constexpr (TWC)
+      PL::fft_tc(v, sm, t, d, tc);
+    else
+      PL::fft(v, sm, t, d);
+  }
+};
+
+template <class PL, int MAXT, int MINB, bool TWC = false>
 __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDesc<typename PL::Scalar> d) {
+  using TCC = TwCache<PL, TWC>;
   using T = typename PL::Scalar;
   using V = cplx<T>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L;
@@ -303,7 +344,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   V* ybuf = sbuf + L;
   const int nv = a.nvalid;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ybuf + ((nv + 1) & ~1));
+  uint32_t* taddr_s = reinterpret_cast<uint32_t*>(bars + 2);
   const int t = threadIdx.x;
+  TCC::alloc(taddr_s, t);
   const int kx = blockIdx.x, b = blockIdx.y;
   // layer split (gridDim.z > 1): this CTA sums layers [r0, r1) and adds its
   // part of W atomically (two splits onto a zeroed W: exact and order-free)
@@ -326,6 +369,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
     tma_load(sbuf, Sb, sbytes, &bars[1], spol);
   }
   __syncthreads();
+  const TmemTwCache tc = TCC::setup(taddr_s, t, d);
   V acc[E], v[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = mkc<V>(T(0), T(0));
@@ -342,7 +386,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
       mbar_arrive_expect_tx(&bars[0], ybytes);
       tma_load(ybuf, Yb + (long long)(r + 1) * a.y_rstride, ybytes, &bars[0], pol);
     }
-    PL::fft(v, sm, t, d);
+    TCC::fft(v, sm, t, d, tc);
     mbar_wait(&bars[1], r & 1);
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -359,7 +403,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   }
 #pragma unroll
   for (int k = 0; k < E; ++k) acc[k] = conjv(acc[k]);
-  PL::fft(acc, sm, t, d);
+  TCC::fft(acc, sm, t, d, tc);
+  TCC::release(taddr_s, t);
   V* wc = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
@@ -377,8 +422,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_fwd_tma(ColFwdArgs a, FFTDes
   }
 }
 
-template <class PL, int MAXT, int MINB>
+template <class PL, int MAXT, int MINB, bool TWC = false>
 __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDesc<typename PL::Scalar> d) {
+  using TCC = TwCache<PL, TWC>;
   using T = typename PL::Scalar;
   using V = cplx<T>;
   constexpr int E = PL::E, NT = PL::NT, L = PL::L;
@@ -387,7 +433,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
   V* sm = reinterpret_cast<V*>(smraw);
   V* sbuf = sm + Ls;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + L);
+  uint32_t* taddr_s = reinterpret_cast<uint32_t*>(bars + 1);
   const int t = threadIdx.x;
+  TCC::alloc(taddr_s, t);
   const int kx = blockIdx.x, b = blockIdx.y;
   const int r0 = (a.K * (int)blockIdx.z) / (int)gridDim.z, K = (a.K * ((int)blockIdx.z + 1)) / (int)gridDim.z - r0;
   const uint32_t sbytes = L * sizeof(V);
@@ -411,7 +459,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
     dh[k] = j < a.nvalid ? dc[j] : mkc<V>(T(0), T(0));
   }
   __syncthreads();
-  PL::fft(dh, sm, t, d);
+  const TmemTwCache tc = TCC::setup(taddr_s, t, d);
+  TCC::fft(dh, sm, t, d, tc);
   V* Wb = static_cast<V*>(a.W) + (long long)b * a.w_bstride + (long long)kx * a.ldw +
           (long long)r0 * a.w_rstride;
   const long long qstride = 1;
@@ -429,7 +478,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
       mbar_arrive_expect_tx(&bars[0], sbytes);
       tma_load(sbuf, Sb + (long long)(r + 1) * a.s_rstride, sbytes, &bars[0], spol);
     }
-    PL::fft(v, sm, t, d);
+    TCC::fft(v, sm, t, d, tc);
     V* wc = Wb + (long long)r * a.w_rstride;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
@@ -437,6 +486,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_col_tra_tma(ColTraArgs a, FFTDes
       if (q < a.nout) wc[q * qstride] = conjv(v[k]);
     }
   }
+  TCC::release(taddr_s, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -1078,6 +1128,13 @@ bool c2r_mirror_ok() {
 }
 #define C2R_MIRROR_PAD(T) (sizeof(T) == 8 ? 8 : 16)  // bank-searched pad of the 8/16/16 exchanges
 
+// loop-invariant pass twiddles of the TMA column stages in TMEM (fft.cuh TmemTwCache);
+// BTTB_TW_TMEM=0 generates them per transform instead
+bool tw_tmem_ok() {
+  static const bool on = env_flag("BTTB_TW_TMEM", true);
+  return on;
+}
+
 bool tma_ok() {
   static const bool ok = getenv("BTTB_NO_TMA") == nullptr;
   return ok;
@@ -1347,8 +1404,10 @@ cudaError_t launch_col_fwd(const ColFwdArgs& a, const FFTDesc<T>& d, int E, cuda
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.nvalid * esz) % 16 == 0 && (a.ldy * esz) % 16 == 0 && (a.y_rstride * esz) % 16 == 0 &&
           (a.y_bstride * esz) % 16 == 0 && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
-        auto kern = k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb>;
-        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L + ((a.nvalid + 1) & ~1)) * esz + 16;
+        constexpr bool twc_ok = PL::kPerPass && PL::NT % 32 == 0 && PL::NT <= 128 && (PL::E == 8 || PL::E == 16);
+        auto kern = (twc_ok && tw_tmem_ok()) ? k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb, twc_ok>
+                                             : k_col_fwd_tma<PL, Shape<PL>::col_threads, Shape<PL>::tma_minb, false>;
+        const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L + ((a.nvalid + 1) & ~1)) * esz + 32;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
         // two layer halves would add into a zeroed W (exact, order-free); opt-in only
@@ -1397,7 +1456,9 @@ cudaError_t launch_col_tra(const ColTraArgs& a, const FFTDesc<T>& d, int E, cuda
     if constexpr (PL::kStatic && PL::NT >= 32) {
       const size_t esz = sizeof(cplx<T>);
       if (tma_ok() && (a.lds * esz) % 16 == 0 && (a.s_rstride * esz) % 16 == 0) {
-        auto kern = k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tra_minb>;
+        constexpr bool twc_ok = PL::kPerPass && PL::NT % 32 == 0 && PL::NT <= 128 && (PL::E == 8 || PL::E == 16);
+        auto kern = (twc_ok && tw_tmem_ok()) ? k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tra_minb, twc_ok>
+                                             : k_col_tra_tma<PL, Shape<PL>::col_threads, Shape<PL>::tra_minb, false>;
         const size_t smem = (size_t)(((PL::slots(d.L) + 1) & ~1) + d.L) * esz + 16;
         cudaError_t e = set_smem(kern, smem);
         if (e != cudaSuccess) return e;
