@@ -694,6 +694,17 @@ def run_ours(a):
     B_apply = algorithmic_bytes(og, bsz, batch)
     achieved = 2 * B_apply / (ms * 1e-3) / 1e9
     traffic, traffic_src = measured_traffic(cfg, a.dtype)
+    # second floor of the fp64 step: its FP64 thread instructions at the pipe's
+    # peak issue rate (committed ncu capture of the same kernel sources)
+    fp64_rec, _ = profile_record(f"{cfg}_{a.dtype}_fp64_pipe") if world == 1 else (None, None)
+    fp64_floor = None
+    if fp64_rec:
+        fp64_floor = {"floor_ms_per_step": fp64_rec["floor_ms_per_step"],
+                      "fp64_thread_inst_per_step": fp64_rec["fp64_thread_inst_per_step"],
+                      "pipe_busy_frac": fp64_rec["floor_ms_per_step"] / ms,
+                      "profile": fp64_rec.get("profile"),
+                      "note": "DADD + DMUL + DFMA thread instructions of one step / (148 SMs x 64 lanes per cycle); "
+                              "the HBM floor of the algorithmic bytes is %.2f ms" % (2 * B_apply / peak / 1e6)}
     cpu = None
     parity = None
     if not a.no_cpu_baseline and world == 1:
@@ -750,8 +761,9 @@ def run_ours(a):
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "frac_of_8TBs_nameplate": achieved / 8000.0,
                      "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_apply": B_apply,
-                     "kernel": "fused operator (row R2C -> column FFT*S accumulate -> column IFFT -> row C2R)"},
+                     "algorithmic_bytes_per_apply": B_apply, "fp64_pipe": fp64_floor,
+                     "kernel": "operator step (row R2C -> column FFT*S accumulate -> column IFFT -> row C2R; both "
+                               "directions), dominant kernels k_col_fwd_tma / k_col_tra_tma"},
         "fwd_ms": fwd_ms, "tra_ms": tra_ms, "build_s": t_build,
         "fwd_voxels_per_s": batch * grid.n / (fwd_ms * 1e-3),
         "tra_voxels_per_s": batch * grid.n / (tra_ms * 1e-3),

@@ -76,6 +76,36 @@ def full_metrics(path):
     return out
 
 
+def fp64_floor(path):
+    """FP64 thread instructions (DADD + DMUL + DFMA, predicated on) per captured
+    kernel and the time they take on the FP64 pipe at its peak issue rate
+    (ncu's own peak: sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained
+    per cycle, 148 SMs x 64 lanes on B200), at the measured SM clock."""
+    rows = list(csv.reader(open(path)))
+    if len(rows) < 3:
+        return []
+    hdr = rows[0]
+
+    def val(r, k):
+        return float(r[hdr.index(k)].replace(",", "")) if k in hdr and r[hdr.index(k)] not in ("", "n/a") else None
+
+    out = []
+    for r in rows[2:]:
+        per = [val(r, f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed")
+               for op in ("dadd", "dmul", "dfma")]
+        cyc = val(r, "smsp__cycles_elapsed.avg")
+        peak = val(r, "sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained")
+        dur = val(r, "gpu__time_duration.sum")
+        if None in per or not cyc or not peak or not dur:
+            continue
+        inst = sum(per) * cyc
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").split("<")[0]
+        out.append({"kernel": name, "grid": r[hdr.index("Grid Size")], "duration_ms": dur, "fp64_thread_inst": inst,
+                    "dadd": per[0] * cyc, "dmul": per[1] * cyc, "dfma": per[2] * cyc,
+                    "floor_ms": inst / peak / (cyc / dur), "peak_per_cycle": peak})
+    return out
+
+
 def main(src, tag):
     os.makedirs(PROF, exist_ok=True)
     lines = [f"# Profile summary `{tag}` (tools/profile_round.sh; B200, clocks not locked)", ""]
@@ -133,6 +163,30 @@ def main(src, tag):
         for name, vals in full_metrics(fpath):
             lines.append(f"* `{name}`: " + ", ".join(f"{k} {v}" for k, v in vals.items()))
         lines.append("")
+        fl = fp64_floor(fpath)
+        if fl:
+            lines += ["## FP64 instruction floor (same capture: one C4 fp64 step)", "",
+                      "FP64 thread instructions per kernel (DADD + DMUL + DFMA, predicated on) and the time they "
+                      "occupy the FP64 pipe at ncu's peak issue rate (%d thread instructions per cycle = 148 SMs x 64 "
+                      "lanes) at the capture's SM clock." % int(fl[0]["peak_per_cycle"]), "",
+                      "| kernel | grid | ms | FP64 thread inst (G) | DADD / DMUL / DFMA (G) | floor ms | pipe busy |",
+                      "|---|---|---|---|---|---|---|"]
+            for k in fl:
+                lines.append(f"| {k['kernel']} | {k['grid']} | {k['duration_ms']:.3f} | {k['fp64_thread_inst'] / 1e9:.2f} | "
+                             f"{k['dadd'] / 1e9:.2f} / {k['dmul'] / 1e9:.2f} / {k['dfma'] / 1e9:.2f} | "
+                             f"{k['floor_ms']:.3f} | {k['floor_ms'] / k['duration_ms']:.2f} |")
+            tot_i = sum(k["fp64_thread_inst"] for k in fl)
+            tot_f = sum(k["floor_ms"] for k in fl)
+            tot_d = sum(k["duration_ms"] for k in fl)
+            lines += [f"| step | | {tot_d:.3f} | {tot_i / 1e9:.2f} | | {tot_f:.3f} | {tot_f / tot_d:.2f} |", "",
+                      f"One step issues {tot_i / 1e9:.1f} G FP64 thread instructions: {tot_f:.2f} ms of the FP64 pipe at "
+                      "100% -- beside the HBM floor of the algorithmic bytes (2 x 5.124 GB / 6.55 TB/s = 1.56 ms) "
+                      "the step has a second, slightly higher floor.", ""]
+            traffic["C4_f64_fp64_pipe"] = {"fp64_thread_inst_per_step": tot_i, "floor_ms_per_step": tot_f,
+                                           "peak_thread_inst_per_cycle": fl[0]["peak_per_cycle"], "profile": tag,
+                                           "csrc_sha": csrc_digest(),
+                                           "how": "ncu --set full: (dadd + dmul + dfma thread instructions per cycle) x "
+                                                  "cycles of every kernel of one step / peak issue rate"}
     f32path = os.path.join(src, "full_f32_raw.csv")
     if os.path.exists(f32path):
         lines += ["## ncu --set full (fp32 row kernels of one C4 step)", ""]
