@@ -158,3 +158,25 @@ def test_cli_bench_rejects_bad_problem_index(capsys):
 
     assert cli.main(["bench", "--problems", "13"]) == 2
     assert "unknown problem index 13" in capsys.readouterr().err
+
+
+def test_bench_profile_figures_are_tied_to_the_kernel_sources(tmp_path, monkeypatch):
+    """bench.py reports a committed ncu figure (DRAM traffic, FP64-pipe floor)
+    only while the CUDA sources hash to the digest the profile was taken on."""
+    import json
+
+    import bench
+
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    cur = bench.csrc_digest()
+    (prof / "traffic.json").write_text(json.dumps({
+        "C4_f64": {"bytes_per_apply": 9.5e9, "profile": "rX", "csrc_sha": cur},
+        "C4_f32": {"bytes_per_apply": 4.7e9, "profile": "rOld", "csrc_sha": "0" * 16}}))
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.setattr(bench, "csrc_digest", lambda: cur)
+    val, src = bench.measured_traffic("C4", "f64")
+    assert val == 9.5e9 and src["profile"] == "rX" and not src.get("stale")
+    val, src = bench.measured_traffic("C4", "f32")
+    assert val is None and src["stale"] is True
+    assert bench.profile_record("missing") == (None, None)
