@@ -167,6 +167,17 @@ template <class T> __host__ __device__ __forceinline__ int team_slots(int L) { r
 template <int PAD> __host__ __device__ __forceinline__ int pad_slot(int i) {
   return i + (int)((unsigned)i / (unsigned)PAD);
 }
+// pad_slot(base + c * STEP) for a compile-time c, given b0 = pad_slot(base):
+// when STEP is a multiple of PAD the slot is affine in c (the quotient moves by
+// exactly c * STEP / PAD), so the access takes an immediate offset instead of
+// its own address arithmetic (the integer pipe runs at half the FP32 rate and
+// binds the fp32 row kernels together with it).
+template <int PAD, int STEP> __host__ __device__ __forceinline__ int pad_slot_at(int b0, int base, int c) {
+  if constexpr (STEP % PAD == 0)
+    return b0 + c * (STEP + STEP / PAD);
+  else
+    return pad_slot<PAD>(base + c * STEP);
+}
 
 // Plan for one transform length, passed by value to kernels.
 template <class T>
@@ -561,9 +572,22 @@ __device__ __forceinline__ void spass_store(const cplx<T> (&v)[E], cplx<T>* sm, 
     const int j = t + NT * b;
     const int k = j % NS;
     const int base = (j - k) * R + k;
+    const int b0 = pad_slot<PAD>(base);
     sfor<0, R>([&](auto rc) {
       constexpr int r = decltype(rc)::value;
-      if (active) sm[pad_slot<PAD>(base + r * NS)] = v[b + r * NB];
+      int slot;
+      if constexpr (NS == 1 && PAD % R == 0) {
+        // first pass: base = j * R is a multiple of R, so with R | PAD the
+        // butterfly's R consecutive slots never cross a pad boundary
+        slot = b0 + r;
+      } else if constexpr (NS % PAD != 0 && PAD % NS == 0 && (NS * R) % PAD == 0) {
+        // base = (multiple of NS * R, hence of PAD) + k with k < NS <= PAD and NS | PAD:
+        // (k + r * NS) / PAD = (r * NS) / PAD, so the slot is b0 plus a constant
+        slot = b0 + r * NS + (r * NS) / PAD;
+      } else {
+        slot = pad_slot_at<PAD, NS>(b0, base, r);
+      }
+      if (active) sm[slot] = v[b + r * NB];
     });
   });
 }
@@ -602,9 +626,10 @@ __device__ __forceinline__ void sfft_c(cplx<T> (&v)[E], cplx<T>* sm, int t, cons
     sync();
     spass_store<T, E, R, NS, NT, PAD>(v, sm, t, active);
     sync();
+    const int t0 = pad_slot<PAD>(t);
 #pragma unroll
     for (int s = 0; s < E; ++s)
-      if (active) v[s] = sm[pad_slot<PAD>(t + NT * s)];
+      if (active) v[s] = sm[pad_slot_at<PAD, NT>(t0, t, s)];
     sfft_c<T, E, L, PAD, PP, (NS > 1 ? OFF + (R - 1) * NS : OFF), NS * R,
            (NS > 1 ? TOFF + (E / R) * tw_cols<cplx<T>, R>() : TOFF), TwC, Rest...>(v, sm, t, tw, tc, active,
                                                                                   NoHook{}, sync);

@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_row_r2c(RowR2CArgs a, FFTDesc<ty
   const int s = blockIdx.y;
   const int q0 = blockIdx.x * 2 * P;
   const int qa = q0 + 2 * c, qb = qa + 1;
-  const T* in = static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride +
-                (long long)(s % a.spb) * a.in_sstride;
+  const T* in = static_cast<const T*>(a.in) + (long long)((unsigned)s / (unsigned)a.spb) * a.in_bstride +
+                (long long)((unsigned)s % (unsigned)a.spb) * a.in_sstride;
   const bool va = qa < a.nrows, vb = qb < a.nrows;
   const T* ra = in + (long long)(va ? qa : 0) * a.ld_in;
   const T* rb = in + (long long)(vb ? qb : 0) * a.ld_in;
@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_row_c2r(RowC2RArgs a, FFTDesc<ty
   PL::fft(v, sm, t, d);
   const int ja = j0 + 2 * c, jb = ja + 1;
   const bool va = ja < a.nrows, vb = jb < a.nrows;
-  T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
+  T* out = static_cast<T*>(a.out) + (long long)((unsigned)s / (unsigned)a.spb) * a.out_bstride +
+           (long long)((unsigned)s % (unsigned)a.spb) * a.out_sstride;
   T* oa = out + (long long)(va ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : 0) * a.ld_out;
 #pragma unroll
@@ -659,8 +660,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
   V* sm = reinterpret_cast<V*>(smraw) + (long long)c * RT::slots((PL::slots(L) + 1) & ~1);
   const int t = threadIdx.x - c * NT, s = blockIdx.y, qa = 2 * (blockIdx.x * TEAMS + c), qb = qa + 1;
   const bool active = qa < a.nrows;
-  const T* in = static_cast<const T*>(a.in) + (long long)(s / a.spb) * a.in_bstride +
-                (long long)(s % a.spb) * a.in_sstride;
+  const T* in = static_cast<const T*>(a.in) + (long long)((unsigned)s / (unsigned)a.spb) * a.in_bstride +
+                (long long)((unsigned)s % (unsigned)a.spb) * a.in_sstride;
   const bool vb = qb < a.nrows;
   const T* ra = in + (long long)(active ? qa : 0) * a.ld_in;
   const T* rb = in + (long long)(vb ? qb : qa) * a.ld_in;
@@ -686,9 +687,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
     const int j1 = t == 0 ? 128 : 256 - t;
     V u0[8], u1[8];
 #pragma unroll
+    const int s0 = pad_slot<PL::kPad>(t), s1 = pad_slot<PL::kPad>(j1);
     for (int r = 0; r < 8; ++r) {
-      u0[r] = sm[pad_slot<PL::kPad>(t + 256 * r)];
-      u1[r] = sm[pad_slot<PL::kPad>(j1 + 256 * r)];
+      u0[r] = sm[pad_slot_at<PL::kPad, 256>(s0, t, r)];
+      u1[r] = sm[pad_slot_at<PL::kPad, 256>(s1, j1, r)];
     }
     V w[8];
     gen_twiddles<V, 8, 256>(w, PL::table(d) + 15 * 16, t);  // w[r] = w_2048^(r t)
@@ -850,7 +852,8 @@ __global__ void __launch_bounds__(MAXT, MINB)
   }
   PL::fft(v, sm, t, d);
   const bool vb = jb < a.nrows;
-  T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
+  T* out = static_cast<T*>(a.out) + (long long)((unsigned)s / (unsigned)a.spb) * a.out_bstride +
+           (long long)((unsigned)s % (unsigned)a.spb) * a.out_sstride;
   T* oa = out + (long long)(active ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
   const int na = active ? a.nout : 0, nb = vb ? a.nout : 0;  // one compare per store
@@ -949,18 +952,23 @@ __global__ void __launch_bounds__(MAXT, MINB)
   dft<8>(u0);  // pass 1 (NS = 1): no twiddles
   dft<8>(u1);
   __syncthreads();  // every thread has read the tile: the exchange may overwrite it
+  // 8 consecutive slots from a multiple of 8 never cross a pad boundary (PADC = 8 or 16)
+  static_assert(PADC % 8 == 0, "mirrored C2R: pad of the 8/16/16 exchanges");
+  const int q0 = pad_slot<PADC>(8 * t), q1 = pad_slot<PADC>(8 * j1);
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    sm[pad_slot<PADC>(8 * t + r)] = u0[r];
-    sm[pad_slot<PADC>(8 * j1 + r)] = u1[r];
+    sm[q0 + r] = u0[r];
+    sm[q1 + r] = u1[r];
   }
   __syncthreads();
   V v[E];
+  const int t0 = pad_slot<PADC>(t);
 #pragma unroll
-  for (int k = 0; k < E; ++k) v[k] = sm[pad_slot<PADC>(t + NT * k)];
+  for (int k = 0; k < E; ++k) v[k] = sm[pad_slot_at<PADC, NT>(t0, t, k)];
   sfft<T, E, L, PADC, true, 0, 8, 16, 16>(v, sm, t, static_cast<const V*>(a.tw_816));
   const bool vb = jb < a.nrows;
-  T* out = static_cast<T*>(a.out) + (long long)(s / a.spb) * a.out_bstride + (long long)(s % a.spb) * a.out_sstride;
+  T* out = static_cast<T*>(a.out) + (long long)((unsigned)s / (unsigned)a.spb) * a.out_bstride +
+           (long long)((unsigned)s % (unsigned)a.spb) * a.out_sstride;
   T* oa = out + (long long)(active ? ja : 0) * a.ld_out;
   T* ob = out + (long long)(vb ? jb : ja) * a.ld_out;
   const int na = active ? a.nout : 0, nb = vb ? a.nout : 0;  // one compare per store
