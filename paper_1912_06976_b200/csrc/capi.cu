@@ -348,6 +348,8 @@ struct bttb_plan_s {
   DevBuf ain[kRing], aout[kRing];
   cudaEvent_t ev_h2d[kRing] = {}, ev_in_free[kRing] = {}, ev_out_ready[kRing] = {}, ev_out_free[kRing] = {};
   cudaEvent_t ev_call = nullptr;
+  static constexpr int kHostChunks = 4;  // layer ranges of the chunked BTTB_HOST_PTR path
+  cudaEvent_t ev_chunk[kHostChunks] = {};
   int ring = 0;
   int64_t last_K = 0, last_G = 0, last_launches = 0;
   std::mutex mu;
@@ -560,10 +562,16 @@ int run_generic(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch,
   return BTTB_OK;
 }
 
+// [L0, L1): the plan's layers this call covers (default all).  A partial range
+// (the chunked host path below: batch 1, whole product) adds its layers to the
+// station half spectrum W of the earlier ranges (forward; the row inverse runs
+// with the last range) or fills its layers of the output (transpose; the data
+// half spectrum is built with the first range and kept in the workspace).
 template <class T>
 int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, cudaStream_t st,
-              int stage = BTTB_STAGE_ALL) {
+              int stage = BTTB_STAGE_ALL, int64_t L0 = 0, int64_t L1 = -1) {
   if (p->generic) return run_generic<T>(p, mode, x, y, batch, st, stage);
+  if (L1 < 0) L1 = p->nzl;
   const bool rows_in = stage != BTTB_STAGE_FROM_SPECTRUM, rows_out = stage != BTTB_STAGE_TO_SPECTRUM;
   using V = cplx<T>;
   const FFTDesc<T> dx = p->fx.desc<T>(), dy = p->fy.desc<T>();
@@ -581,7 +589,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
   if ((rc = p->work.ensure(ybytes + wbytes))) return rc;
   p->last_K = K;
   p->last_G = G;
-  int64_t launches = 0;
+  int64_t launches = L0 > 0 ? p->last_launches : 0;
   V* Yb = static_cast<V*>(p->work.p);
   V* Wb = reinterpret_cast<V*>(static_cast<char*>(p->work.p) + ybytes);
   const V* S = static_cast<const V*>(p->spectra);
@@ -594,8 +602,8 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       V* Wg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b0 * Hx * sy
               : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b0 * Hx * sy
                                                   : Wb;
-      for (int64_t r0 = 0; rows_in && r0 < p->nzl; r0 += K) {
-        const int k = (int)std::min<int64_t>(K, p->nzl - r0);
+      for (int64_t r0 = L0; rows_in && r0 < L1; r0 += K) {
+        const int k = (int)std::min<int64_t>(K, L1 - r0);
         RowR2CArgs ra{};
         ra.in = xin + r0 * n_r;
         ra.in_bstride = nloc;
@@ -630,7 +638,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         CU(launch_col_fwd<T>(ca, dy, p->fy.template E<T>(), st));
         launches += 2;
       }
-      if (!rows_out) continue;
+      if (!rows_out || L1 != p->nzl) continue;
       RowC2RArgs oa{};
       oa.in = Wg;
       oa.in_sstride = (long long)Hx * sy;
@@ -651,7 +659,7 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
       V* Dg = stage == BTTB_STAGE_TO_SPECTRUM     ? static_cast<V*>(y) + b0 * Hx * sy
               : stage == BTTB_STAGE_FROM_SPECTRUM ? const_cast<V*>(static_cast<const V*>(x)) + b0 * Hx * sy
                                                   : Wb;
-      if (rows_in) {
+      if (rows_in && L0 == 0) {
         RowR2CArgs ra{};
         ra.in = static_cast<const T*>(x) + b0 * m;
         ra.in_bstride = m;
@@ -669,8 +677,8 @@ int run_apply(bttb_plan_s* p, int mode, const void* x, void* y, int64_t batch, c
         launches += 1;
       }
       T* yout = static_cast<T*>(y) + b0 * nloc;
-      for (int64_t r0 = 0; rows_out && r0 < p->nzl; r0 += K) {
-        const int k = (int)std::min<int64_t>(K, p->nzl - r0);
+      for (int64_t r0 = L0; rows_out && r0 < L1; r0 += K) {
+        const int k = (int)std::min<int64_t>(K, L1 - r0);
         ColTraArgs ca{};
         ca.D = Dg;
         ca.d_bstride = (long long)Hx * sy;
@@ -743,6 +751,10 @@ void destroy_plan(bttb_plan_s* p) {
       if (ev) cudaEventDestroy(ev);
   }
   if (p->ev_call) cudaEventDestroy(p->ev_call);
+  for (cudaEvent_t& ev : p->ev_chunk) {
+    if (ev) cudaEventDestroy(ev);
+    ev = nullptr;
+  }
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   p->hin.release();
@@ -1001,6 +1013,12 @@ int bttb_plan_destroy(bttb_plan* plan) {
   return BTTB_OK;
 }
 
+// layer-chunked overlap of copies and compute in the synchronous host path; BTTB_HOST_CHUNKS=0 off
+static bool host_chunks_ok() {
+  static const bool on = !(getenv("BTTB_HOST_CHUNKS") && atoi(getenv("BTTB_HOST_CHUNKS")) == 0);
+  return on;
+}
+
 int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, int where, void* stream) {
   g_err.clear();
   if (!p || !x || !y) return fail(BTTB_EINVAL, "null argument");
@@ -1048,6 +1066,51 @@ int bttb_apply(bttb_plan* p, int mode, const void* x, void* y, int64_t batch, in
   }
   const void* xd = x;
   void* yd = y;
+  // BTTB_HOST_PTR with one large model: the copy of one layer range crosses
+  // PCIe while the previous range is computed (forward) / the next range is
+  // computed while this one's result leaves (transpose) -- the synchronous
+  // call hides its ~1.7 ms of C4 compute behind its 1.03 GB copy.
+  constexpr int NC = bttb_plan_s::kHostChunks;
+  if (where == BTTB_HOST_PTR && batch == 1 && !p->generic && p->nzl >= 2 * NC &&
+      (size_t)p->nloc() * esz >= ((size_t)64 << 20) && host_chunks_ok()) {
+    int rc;
+    if ((rc = p->hin.ensure(in_elems * esz)) || (rc = p->hout.ensure(out_elems * esz))) return rc;
+    for (cudaEvent_t& ev : p->ev_chunk)
+      if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    const size_t lbytes = (size_t)p->n_r() * esz;  // one layer of the model
+    auto run = [&](int64_t lo, int64_t hi) {
+      return p->dtype == BTTB_F64 ? run_apply<double>(p, mode, p->hin.p, p->hout.p, 1, p->stream, BTTB_STAGE_ALL, lo, hi)
+                                  : run_apply<float>(p, mode, p->hin.p, p->hout.p, 1, p->stream, BTTB_STAGE_ALL, lo, hi);
+    };
+    if (mode == BTTB_FORWARD) {
+      for (int c = 0; c < NC; ++c) {
+        const int64_t lo = p->nzl * c / NC, hi = p->nzl * (c + 1) / NC;
+        CU(stage_h2d(p->hstage, static_cast<char*>(p->hin.p) + lo * lbytes, static_cast<const char*>(x) + lo * lbytes,
+                     (size_t)(hi - lo) * lbytes, st));
+        CU(cudaEventRecord(p->ev_chunk[c], st));
+        CU(cudaStreamWaitEvent(p->stream, p->ev_chunk[c], 0));
+        if ((rc = run(lo, hi))) return rc;
+      }
+      CU(cudaEventRecord(p->ev_out, p->stream));
+      CU(cudaStreamWaitEvent(st, p->ev_out, 0));
+      CU(stage_d2h(p->hstage, y, p->hout.p, out_elems * esz, st));
+    } else {
+      CU(stage_h2d(p->hstage, p->hin.p, x, in_elems * esz, st));
+      CU(cudaEventRecord(p->ev_in, st));
+      CU(cudaStreamWaitEvent(p->stream, p->ev_in, 0));
+      for (int c = 0; c < NC; ++c) {
+        if ((rc = run(p->nzl * c / NC, p->nzl * (c + 1) / NC))) return rc;
+        CU(cudaEventRecord(p->ev_chunk[c], p->stream));
+      }
+      for (int c = 0; c < NC; ++c) {
+        const int64_t lo = p->nzl * c / NC, hi = p->nzl * (c + 1) / NC;
+        CU(cudaStreamWaitEvent(st, p->ev_chunk[c], 0));
+        CU(stage_d2h(p->hstage, static_cast<char*>(y) + lo * lbytes, static_cast<char*>(p->hout.p) + lo * lbytes,
+                     (size_t)(hi - lo) * lbytes, st));
+      }
+    }
+    return BTTB_OK;
+  }
   if (where == BTTB_HOST_PTR) {
     int rc;
     if ((rc = p->hin.ensure(in_elems * esz)) || (rc = p->hout.ensure(out_elems * esz))) return rc;

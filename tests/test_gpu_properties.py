@@ -327,3 +327,31 @@ def test_pageable_staging_odd_sizes():
             xd = B.apply(st, torch.tensor(v, device="cuda"), "transpose").cpu().numpy()
         np.testing.assert_array_equal(y, yd)
         np.testing.assert_array_equal(xt, xd)
+
+
+def test_host_path_layer_chunked_overlap():
+    """BTTB_HOST_PTR with one large model (>= 64 MB, >= 8 layers) runs in four
+    layer ranges so that copies and compute overlap (capi.cu, bttb_apply):
+    10 C4 layers (80 MB) split 2 / 3 / 2 / 3.  The transpose is bit-identical
+    to the device-pointer path (layers are independent); the forward adds four
+    partial station spectra instead of one (rounding order only)."""
+    import torch
+
+    from paper_1912_06976_b200.multiply import apply_into
+
+    og = O.config_grid("C4")
+    params = B.KernelParams.magnetic(*O.CONFIGS["C4"][11])
+    grid = B.make_grid(og.sx, og.sy, og.nz, og.pxl, og.pxr, og.pyl, og.pyr, og.dx, og.dy, og.z)
+    rng = np.random.default_rng(47)
+    with B.build_transform_stack(grid, params, layers=(20, 30)) as st:
+        x = rng.uniform(0.0, 0.05, st.n_local)
+        v = rng.normal(0.0, 1.0, og.m)
+        y = np.empty(og.m)
+        xt = np.empty(st.n_local)
+        for _ in range(2):  # twice: the retained workspace state must not leak between calls
+            apply_into(st, "forward", x.ctypes.data, y.ctypes.data, 1, host=True)
+            apply_into(st, "transpose", v.ctypes.data, xt.ctypes.data, 1, host=True)
+        yd = B.apply(st, torch.tensor(x, device="cuda"), "forward").cpu().numpy()
+        xd = B.apply(st, torch.tensor(v, device="cuda"), "transpose").cpu().numpy()
+    np.testing.assert_array_equal(xt, xd)
+    assert O.rel_l2(yd, y) <= 1e-14
