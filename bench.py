@@ -640,7 +640,8 @@ def run_ours(a):
             e2e["reference_api"] = {
                 "value": grid.n / t_ref, "ms_per_step": 1e3 * t_ref,
                 "path": "apply(stack, numpy_array, mode) as the reference's callers make it: pageable numpy "
-                        "arrays, synchronous host path (BTTB_HOST_PTR), new output array per call"}
+                        "arrays, synchronous host path (BTTB_HOST_PTR: pinned chunk ring, four layer ranges whose "
+                        "copies and compute overlap), new output array per call"}
 
     # max over ranks
     vals = torch.tensor([ms, fwd_ms, tra_ms, t_build], device=dev, dtype=torch.float64)
